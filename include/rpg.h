@@ -1,0 +1,211 @@
+/*
+ * rpg.h — C ABI of the B200 rational-program evaluator (librpgpu.so).
+ *
+ * The reference (`ratprog`, arXiv 1906.00142 / KLARAPTOR restatement) has no
+ * FFI: its hot path is a header-only C++ API.  This header is the thin,
+ * plain-pointer boundary that sits under the C++ drop-in
+ * (`ratprog::pipe::search_optimal` & co.) and that any
+ * ctypes / cgo / JNI binding would use.  No torch or CUDA types appear here;
+ * every buffer passed to a non-`_device` entry point is caller-owned HOST
+ * memory, copied in and out, and no pointer is retained after the call
+ * returns (the reference returns by value).
+ *
+ * Entry points and the reference interface each one replaces:
+ *
+ *   rpg_plan_create        — the one-time setup done by
+ *                            pipe::generate_rp + make_binding_plan
+ *                            (pipeline.hpp:233-255, 482-516) and
+ *                            perf::check_metric_spec (perfmodel.hpp:428-456):
+ *                            validates the metric spec / profile / space and
+ *                            uploads them to the device once.
+ *   rpg_search_batch       — pipe::search_optimal (pipeline.hpp:575-680),
+ *                            batched over data tuples: per tuple, the winning
+ *                            configuration under the reference's ranking
+ *                            (min Ec, tie group Ec <= best*(1+tol), max
+ *                            occupancy, then Ec, then lex (bx,by,bz)).
+ *   rpg_evaluate           — the per-config values search_optimal computes
+ *                            before ranking: the program output
+ *                            (ir::evaluate of emit_mwpcwp_rp,
+ *                            perfmodel.hpp:648-834; -1 sentinel when the
+ *                            program branches to `infeasible`), the occupancy
+ *                            used for tie-breaking and the case tag
+ *                            (pipeline.hpp:623-652).
+ *   rpg_search             — one-shot create + search_batch + destroy.
+ *   rpg_fit_rational       — poly::fit_rational (polyfit.hpp:337-427).
+ *
+ * Error convention: 0 on success, a negative RPG_E_* code otherwise, with a
+ * NUL-terminated message written to `err` (may be NULL).  Messages reuse the
+ * reference's wording so the C++ shim can rethrow the same exception types.
+ */
+#ifndef RPG_H_
+#define RPG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RPG_ABI_VERSION 1
+
+#define RPG_MAX_VARS 8
+#define RPG_N_METRICS 7
+
+/* Metric slots, in the order evaluate_metrics reads them
+ * (perfmodel.hpp:468-476). */
+enum {
+  RPG_METRIC_REGS = 0,         /* regs_per_thread */
+  RPG_METRIC_SHARED = 1,       /* shared_words_per_block */
+  RPG_METRIC_COMP = 2,         /* comp_insts_per_thread */
+  RPG_METRIC_UNCOAL = 3,       /* uncoal_mem_insts_per_thread */
+  RPG_METRIC_COAL = 4,         /* coal_mem_insts_per_thread */
+  RPG_METRIC_SYNCH = 5,        /* synch_insts_per_block */
+  RPG_METRIC_TOTAL_BLOCKS = 6  /* total_blocks */
+};
+
+/* Variable kinds (model variable order is data-driven, perfmodel.hpp:416-420):
+ * k >= 0 is data parameter D(k+1); negative codes are block dimensions. */
+enum { RPG_VAR_BX = -1, RPG_VAR_BY = -2, RPG_VAR_BZ = -3 };
+
+/* perf::CaseTag (perfmodel.hpp:273) plus "-" for rows whose direct-path
+ * diagnostics threw (pipeline.hpp:637-647). */
+enum {
+  RPG_CASE_BOTH_SATURATED = 0,
+  RPG_CASE_CWP_BOUND = 1,
+  RPG_CASE_MWP_BOUND = 2,
+  RPG_CASE_UNKNOWN = 3
+};
+
+/* perf::RepMode (perfmodel.hpp:271). */
+enum { RPG_REP_REAL = 0, RPG_REP_CEIL = 1 };
+
+/* Arithmetic mode of the evaluator.
+ *   RPG_ARITH_EXACT: IEEE mul/add in the reference's basis order, no FMA
+ *                    contraction — bit-identical to oracle O1.
+ *   RPG_ARITH_FAST:  per-data-tuple collapse of the data-parameter part of
+ *                    every polynomial and DFMA Horner evaluation of the
+ *                    block-dimension part (bit-identical to O1's FAST twin). */
+enum { RPG_ARITH_EXACT = 0, RPG_ARITH_FAST = 1 };
+
+enum {
+  RPG_OK = 0,
+  RPG_E_INVALID = -1,      /* std::invalid_argument */
+  RPG_E_MODEL = -2,        /* perf::ModelError */
+  RPG_E_PROFILE = -3,      /* perf::ProfileError */
+  RPG_E_CUDA = -4,         /* device / driver failure */
+  RPG_E_NO_FEASIBLE = -5,  /* pipe::NoFeasibleConfig (single-tuple calls) */
+  RPG_E_PIPELINE = -6,     /* pipe::PipelineError */
+  RPG_E_FIT = -7           /* poly::DegenerateFit / SvdFailure */
+};
+
+/* perf::DeviceProfile, same fields and order (perfmodel.hpp:50-65). */
+typedef struct {
+  int64_t R_max, Z_max, T_max, B_max, W_max, num_SM;
+  double freq_GHz, mem_latency_cycles, departure_del_coal_cycles,
+      departure_del_uncoal_cycles, mem_bandwidth_GBps, issue_cycles;
+  int64_t load_bytes_per_warp, uncoal_per_mw;
+} rpg_profile;
+
+/* One polynomial in sparse "AltArr-like" form: term k is
+ * coef[k] * prod_v x_v^exps[k*n_vars+v], terms in graded-lex basis order
+ * (polyfit.hpp:50-73).  The order fixes the FP summation order. */
+typedef struct {
+  int32_t n_terms;
+  int32_t reserved;
+  const double* coef;
+  const uint8_t* exps;
+} rpg_poly;
+
+/* One metric source: a constant or a fitted p/q (perfmodel.hpp:416-426). */
+typedef struct {
+  int32_t is_const;
+  int32_t reserved;
+  double value;
+  rpg_poly num, den;
+} rpg_metric;
+
+/* perf::MetricSpec: variables (D1..Dd, bx, by[, bz] in any order) and the
+ * seven metric sources indexed by RPG_METRIC_*. */
+typedef struct {
+  int32_t n_vars;
+  int32_t var_kind[RPG_MAX_VARS];
+  rpg_metric metric[RPG_N_METRICS];
+} rpg_model;
+
+/* perf::LaunchConfig (perfmodel.hpp:79-84). */
+typedef struct {
+  int64_t bx, by, bz;
+} rpg_config;
+
+/* pipe::SearchOptions subset (pipeline.hpp:438-452). */
+typedef struct {
+  int32_t rep_mode;       /* RPG_REP_* */
+  int32_t arith;          /* RPG_ARITH_* */
+  double tie_rel_tol;     /* default 1e-12 */
+  double regs_per_thread; /* occupancy context on DenominatorNearZero */
+  double shared_words_per_block;
+} rpg_options;
+
+/* Per-tuple search result (the head of pipe::SearchResult::ranking plus its
+ * counters).  cfg_idx = -1 when no configuration is feasible. */
+typedef struct {
+  double ec;          /* estimated cycles of the winner */
+  double best_ec;     /* minimum Ec over the tuple (tie-group anchor) */
+  int32_t cfg_idx;    /* index into the plan's configuration space */
+  int32_t ties;       /* size of the leading tie group */
+  int32_t n_feasible; /* evaluated - infeasible */
+  int32_t b_active;   /* resident blocks per SM of the winner */
+  int32_t w_active;   /* resident warps per SM of the winner */
+  int32_t w_occ;      /* warps behind the winner's occupancy (w_occ/W_max) */
+  int32_t case_tag;   /* RPG_CASE_* of the winner */
+  int32_t reserved;
+} rpg_winner;
+
+typedef struct rpg_plan rpg_plan;
+
+const char* rpg_version(void);
+int rpg_device_count(void);
+
+int rpg_plan_create(const rpg_model* model, const rpg_profile* hw,
+                    const rpg_config* space, int64_t n_space,
+                    const rpg_options* opts, int32_t device, rpg_plan** out,
+                    char* err, size_t errlen);
+int rpg_plan_destroy(rpg_plan* plan);
+
+/* data: n_tuples x d int64 data-parameter values (D1..Dd), host memory.
+ * out: n_tuples winners, host memory. */
+int rpg_search_batch(rpg_plan* plan, const int64_t* data, int64_t n_tuples,
+                     int32_t d, rpg_winner* out, char* err, size_t errlen);
+
+/* Same, with device-resident inputs/outputs on the given cudaStream_t
+ * (passed as void*).  Asynchronous: returns after enqueueing. */
+int rpg_search_batch_device(rpg_plan* plan, const int64_t* d_data,
+                            int64_t n_tuples, int32_t d, rpg_winner* d_out,
+                            void* stream, char* err, size_t errlen);
+
+/* Full per-point table, tuple-major (index t*n_space + c).  ec: program
+ * output (-1 sentinel for launch/denominator infeasibility; negative values
+ * are infeasible for the search too).  tag: RPG_CASE_*.  w_occ: occupancy
+ * warps.  Any output pointer may be NULL.  Host memory. */
+int rpg_evaluate(rpg_plan* plan, const int64_t* data, int64_t n_tuples,
+                 int32_t d, double* ec, uint8_t* tag, int32_t* w_occ,
+                 char* err, size_t errlen);
+
+int rpg_evaluate_device(rpg_plan* plan, const int64_t* d_data,
+                        int64_t n_tuples, int32_t d, double* d_ec,
+                        uint8_t* d_tag, int32_t* d_w_occ, void* stream,
+                        char* err, size_t errlen);
+
+/* One-shot convenience for FFI callers. */
+int rpg_search(const rpg_model* model, const rpg_profile* hw,
+               const rpg_config* space, int64_t n_space,
+               const rpg_options* opts, const int64_t* data,
+               int64_t n_tuples, int32_t d, int32_t device, rpg_winner* out,
+               char* err, size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RPG_H_ */

@@ -1,0 +1,223 @@
+"""ctypes mirror of include/rpg.h and the loader for librpgpu.so.
+
+The library is the product: a missing or unloadable ``librpgpu.so`` raises
+``RuntimeError`` — there is no CPU fallback anywhere on this path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import formats as F
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librpgpu.so")
+
+RPG_MAX_VARS = 8
+RPG_N_METRICS = 7
+RPG_VAR_BX, RPG_VAR_BY, RPG_VAR_BZ = -1, -2, -3
+RPG_CASE_BOTH_SATURATED, RPG_CASE_CWP_BOUND, RPG_CASE_MWP_BOUND, RPG_CASE_UNKNOWN = 0, 1, 2, 3
+CASE_NAMES = {0: "both_saturated", 1: "cwp_bound", 2: "mwp_bound", 3: "-"}
+RPG_REP_REAL, RPG_REP_CEIL = 0, 1
+RPG_ARITH_EXACT, RPG_ARITH_FAST = 0, 1
+
+RPG_OK = 0
+RPG_E_INVALID = -1
+RPG_E_MODEL = -2
+RPG_E_PROFILE = -3
+RPG_E_CUDA = -4
+RPG_E_NO_FEASIBLE = -5
+RPG_E_PIPELINE = -6
+RPG_E_FIT = -7
+
+
+class rpg_profile(C.Structure):
+    _fields_ = [(k, C.c_int64 if k in F._COUNT_KEYS else C.c_double)
+                for k in F.PROFILE_KEYS]
+
+
+class rpg_poly(C.Structure):
+    _fields_ = [("n_terms", C.c_int32), ("reserved", C.c_int32),
+                ("coef", C.POINTER(C.c_double)), ("exps", C.POINTER(C.c_uint8))]
+
+
+class rpg_metric(C.Structure):
+    _fields_ = [("is_const", C.c_int32), ("reserved", C.c_int32),
+                ("value", C.c_double), ("num", rpg_poly), ("den", rpg_poly)]
+
+
+class rpg_model(C.Structure):
+    _fields_ = [("n_vars", C.c_int32), ("var_kind", C.c_int32 * RPG_MAX_VARS),
+                ("metric", rpg_metric * RPG_N_METRICS)]
+
+
+class rpg_config(C.Structure):
+    _fields_ = [("bx", C.c_int64), ("by", C.c_int64), ("bz", C.c_int64)]
+
+
+class rpg_options(C.Structure):
+    _fields_ = [("rep_mode", C.c_int32), ("arith", C.c_int32),
+                ("tie_rel_tol", C.c_double), ("regs_per_thread", C.c_double),
+                ("shared_words_per_block", C.c_double)]
+
+
+class rpg_winner(C.Structure):
+    _fields_ = [("ec", C.c_double), ("best_ec", C.c_double),
+                ("cfg_idx", C.c_int32), ("ties", C.c_int32),
+                ("n_feasible", C.c_int32), ("b_active", C.c_int32),
+                ("w_active", C.c_int32), ("w_occ", C.c_int32),
+                ("case_tag", C.c_int32), ("reserved", C.c_int32)]
+
+
+WINNER_DTYPE = np.dtype([("ec", "<f8"), ("best_ec", "<f8"), ("cfg_idx", "<i4"),
+                         ("ties", "<i4"), ("n_feasible", "<i4"),
+                         ("b_active", "<i4"), ("w_active", "<i4"),
+                         ("w_occ", "<i4"), ("case_tag", "<i4"),
+                         ("reserved", "<i4")])
+assert WINNER_DTYPE.itemsize == C.sizeof(rpg_winner) == 48
+CONFIG_DTYPE = np.dtype([("bx", "<i8"), ("by", "<i8"), ("bz", "<i8")])
+
+
+def profile_struct(hw: F.DeviceProfile) -> rpg_profile:
+    s = rpg_profile()
+    for k in F.PROFILE_KEYS:
+        setattr(s, k, getattr(hw, k))
+    return s
+
+
+def options_struct(rep_mode: int = RPG_REP_REAL, arith: int = RPG_ARITH_EXACT,
+                   tie_rel_tol: float = 1e-12, regs_per_thread: float = 0.0,
+                   shared_words_per_block: float = 0.0) -> rpg_options:
+    return rpg_options(rep_mode, arith, tie_rel_tol, regs_per_thread,
+                       shared_words_per_block)
+
+
+def var_kind(name: str) -> int:
+    if name == "bx":
+        return RPG_VAR_BX
+    if name == "by":
+        return RPG_VAR_BY
+    if name == "bz":
+        return RPG_VAR_BZ
+    return int(name[1:]) - 1  # D<k> -> k-1
+
+
+class PackedModel:
+    """An rpg_model plus the numpy buffers its pointers reference.
+
+    ``drop_zero_terms`` mirrors emit_ratfunc (perfmodel.hpp:521): exact-zero
+    coefficients contribute nothing and are skipped."""
+
+    def __init__(self, spec: F.MetricSpec, drop_zero_terms: bool = True):
+        F.check_metric_spec(spec)
+        nv = len(spec.variables)
+        if nv > RPG_MAX_VARS:
+            raise F.ModelError(f"at most {RPG_MAX_VARS} model variables are supported")
+        self.spec = spec
+        self.struct = rpg_model()
+        self.struct.n_vars = nv
+        for i, v in enumerate(spec.variables):
+            self.struct.var_kind[i] = var_kind(v)
+        self._keep: List[np.ndarray] = []
+        for slot, name in enumerate(F.METRIC_SLOTS):
+            m = self.struct.metric[slot]
+            if name in spec.constants:  # constants take priority (perfmodel.hpp:463-465)
+                m.is_const = 1
+                m.value = float(spec.constants[name])
+            else:
+                f = spec.models[name]
+                m.is_const = 0
+                m.num = self._poly(f.num, nv, drop_zero_terms)
+                m.den = self._poly(f.den, nv, drop_zero_terms)
+
+    def _poly(self, p: F.Polynomial, nv: int, drop: bool) -> rpg_poly:
+        keep = [k for k, c in enumerate(p.coeffs) if not (drop and c == 0.0)]
+        coef = np.ascontiguousarray([p.coeffs[k] for k in keep], dtype=np.float64)
+        exps = np.ascontiguousarray([p.basis[k] for k in keep],
+                                    dtype=np.uint8).reshape(len(keep), nv)
+        if any(e > 255 for k in keep for e in p.basis[k]):
+            raise F.ModelError("exponents above 255 are not supported")
+        self._keep += [coef, exps]
+        out = rpg_poly()
+        out.n_terms = len(keep)
+        out.coef = coef.ctypes.data_as(C.POINTER(C.c_double)) if len(keep) else None
+        out.exps = exps.ctypes.data_as(C.POINTER(C.c_uint8)) if len(keep) else None
+        return out
+
+
+def config_array(space: Sequence[Tuple[int, int, int]]) -> np.ndarray:
+    arr = np.zeros(len(space), dtype=CONFIG_DTYPE)
+    if len(space):
+        a = np.asarray(space, dtype=np.int64).reshape(len(space), 3)
+        arr["bx"], arr["by"], arr["bz"] = a[:, 0], a[:, 1], a[:, 2]
+    return arr
+
+
+def ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+_LIB: Optional[C.CDLL] = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Loads librpgpu.so.  Raises if it is absent: the product has no
+    fallback evaluator."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the CUDA evaluator is required; there is no CPU fallback)")
+    lib = C.CDLL(path)
+    errbuf = (C.c_char_p, C.c_size_t)
+    sig = {
+        "rpg_version": (C.c_char_p, ()),
+        "rpg_device_count": (C.c_int, ()),
+        "rpg_plan_create": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
+                                      C.POINTER(rpg_config), C.c_int64,
+                                      C.POINTER(rpg_options), C.c_int32,
+                                      C.POINTER(C.c_void_p)) + errbuf),
+        "rpg_plan_destroy": (C.c_int, (C.c_void_p,)),
+        "rpg_search_batch": (C.c_int, (C.c_void_p, C.POINTER(C.c_int64), C.c_int64,
+                                       C.c_int32, C.c_void_p) + errbuf),
+        "rpg_search_batch_device": (C.c_int, (C.c_void_p, C.c_void_p, C.c_int64,
+                                              C.c_int32, C.c_void_p, C.c_void_p) + errbuf),
+        "rpg_evaluate": (C.c_int, (C.c_void_p, C.POINTER(C.c_int64), C.c_int64,
+                                   C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p) + errbuf),
+        "rpg_evaluate_device": (C.c_int, (C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                          C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p) + errbuf),
+        "rpg_search": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
+                                 C.POINTER(rpg_config), C.c_int64,
+                                 C.POINTER(rpg_options), C.POINTER(C.c_int64),
+                                 C.c_int64, C.c_int32, C.c_int32, C.c_void_p) + errbuf),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = list(args)
+    _LIB = lib
+    return lib
+
+
+EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
+                    "rpg_plan_destroy", "rpg_search_batch",
+                    "rpg_search_batch_device", "rpg_evaluate",
+                    "rpg_evaluate_device", "rpg_search")
+
+
+class RpgError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+def check(code: int, err) -> None:
+    if code != RPG_OK:
+        msg = err.value.decode(errors="replace") if err is not None else ""
+        raise RpgError(code, msg)
