@@ -226,7 +226,7 @@ def gpu_arm(args):
     dev = torch.device("cuda", local)
 
     hw, specs, space = load_workload()
-    opts = S.SearchOptions(arith=args.arith, device=local)
+    opts = S.SearchOptions(arith=args.arith, kernel=args.kernel, device=local)
     plans = {k: S.Plan(specs[k], hw, space, opts) for k in KERNELS}
     n = N_PER_RANK
     lo = N0 + rank * n
@@ -342,7 +342,7 @@ def gpu_arm(args):
                                    "default bounds), dense N sweep, 7262 integer (bx,by) configs, B200 profile",
                        "n_per_gpu": n, "n_range_rank0": [lo, lo + n - 1], "configs": len(space),
                        "kernels": list(KERNELS), "evals_per_gpu_step": evals_per_rank_step,
-                       "arith": args.arith, "parallelism": f"N-axis shard x{world}",
+                       "arith": args.arith, "kernel": args.kernel, "parallelism": f"N-axis shard x{world}",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_tf, "traffic": traffic,
@@ -371,6 +371,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--arith", choices=["exact", "fast"], default="fast")
+    ap.add_argument("--kernel", choices=["specialized", "generic"], default="specialized")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -40,8 +40,10 @@
 #ifndef RPG_H_
 #define RPG_H_
 
+#ifndef __CUDACC_RTC__
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -138,6 +140,14 @@ typedef struct {
   int64_t bx, by, bz;
 } rpg_config;
 
+/* Which device implementation evaluates the points (both are sm_100a CUDA;
+ * both are bit-identical to oracle O1):
+ *   RPG_KERNEL_SPECIALIZED: a kernel generated for this model at plan time
+ *                           (NVRTC, sm_100a): straight-line polynomial code,
+ *                           coefficients as immediates (default);
+ *   RPG_KERNEL_GENERIC:     the ahead-of-time table-driven kernel. */
+enum { RPG_KERNEL_SPECIALIZED = 0, RPG_KERNEL_GENERIC = 1 };
+
 /* pipe::SearchOptions subset (pipeline.hpp:438-452). */
 typedef struct {
   int32_t rep_mode;       /* RPG_REP_* */
@@ -145,6 +155,8 @@ typedef struct {
   double tie_rel_tol;     /* default 1e-12 */
   double regs_per_thread; /* occupancy context on DenominatorNearZero */
   double shared_words_per_block;
+  int32_t kernel;         /* RPG_KERNEL_* */
+  int32_t reserved;
 } rpg_options;
 
 /* Per-tuple search result (the head of pipe::SearchResult::ranking plus its
@@ -196,6 +208,17 @@ int rpg_evaluate_device(rpg_plan* plan, const int64_t* d_data,
                         int64_t n_tuples, int32_t d, double* d_ec,
                         uint8_t* d_tag, int32_t* d_w_occ, void* stream,
                         char* err, size_t errlen);
+
+/* The CUDA source of the specialized kernels a plan compiles for this model
+ * (the B200 counterpart of pipe::emit_c_source, pipeline.hpp:276-433).
+ * Writes up to buflen bytes (NUL-terminated; buf may be NULL) and returns the
+ * full source length, or a negative RPG_E_* code.  With compile != 0 the
+ * source is also compiled for sm_100a with NVRTC (no GPU needed) and
+ * *cubin_bytes (nullable) receives the cubin size. */
+int64_t rpg_emit_cuda_source(const rpg_model* model, const rpg_profile* hw,
+                             const rpg_options* opts, int32_t compile, char* buf,
+                             size_t buflen, int64_t* cubin_bytes, char* err,
+                             size_t errlen);
 
 /* One-shot convenience for FFI callers. */
 int rpg_search(const rpg_model* model, const rpg_profile* hw,

@@ -23,6 +23,7 @@ RPG_CASE_BOTH_SATURATED, RPG_CASE_CWP_BOUND, RPG_CASE_MWP_BOUND, RPG_CASE_UNKNOW
 CASE_NAMES = {0: "both_saturated", 1: "cwp_bound", 2: "mwp_bound", 3: "-"}
 RPG_REP_REAL, RPG_REP_CEIL = 0, 1
 RPG_ARITH_EXACT, RPG_ARITH_FAST = 0, 1
+RPG_KERNEL_SPECIALIZED, RPG_KERNEL_GENERIC = 0, 1
 
 RPG_OK = 0
 RPG_E_INVALID = -1
@@ -61,7 +62,8 @@ class rpg_config(C.Structure):
 class rpg_options(C.Structure):
     _fields_ = [("rep_mode", C.c_int32), ("arith", C.c_int32),
                 ("tie_rel_tol", C.c_double), ("regs_per_thread", C.c_double),
-                ("shared_words_per_block", C.c_double)]
+                ("shared_words_per_block", C.c_double),
+                ("kernel", C.c_int32), ("reserved", C.c_int32)]
 
 
 class rpg_winner(C.Structure):
@@ -90,9 +92,10 @@ def profile_struct(hw: F.DeviceProfile) -> rpg_profile:
 
 def options_struct(rep_mode: int = RPG_REP_REAL, arith: int = RPG_ARITH_EXACT,
                    tie_rel_tol: float = 1e-12, regs_per_thread: float = 0.0,
-                   shared_words_per_block: float = 0.0) -> rpg_options:
+                   shared_words_per_block: float = 0.0,
+                   kernel: int = RPG_KERNEL_SPECIALIZED) -> rpg_options:
     return rpg_options(rep_mode, arith, tie_rel_tol, regs_per_thread,
-                       shared_words_per_block)
+                       shared_words_per_block, kernel, 0)
 
 
 def var_kind(name: str) -> int:
@@ -192,6 +195,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "rpg_evaluate_device": (C.c_int, (C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                           C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_void_p) + errbuf),
+        "rpg_emit_cuda_source": (C.c_int64, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
+                                             C.POINTER(rpg_options), C.c_int32, C.c_char_p,
+                                             C.c_size_t, C.POINTER(C.c_int64)) + errbuf),
         "rpg_search": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
                                  C.POINTER(rpg_config), C.c_int64,
                                  C.POINTER(rpg_options), C.POINTER(C.c_int64),
@@ -208,7 +214,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_plan_destroy", "rpg_search_batch",
                     "rpg_search_batch_device", "rpg_evaluate",
-                    "rpg_evaluate_device", "rpg_search")
+                    "rpg_evaluate_device", "rpg_search", "rpg_emit_cuda_source")
 
 
 class RpgError(RuntimeError):

@@ -1,0 +1,33 @@
+// rpg_jit.h — host interface of the per-model specialized kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "rpg_device.cuh"
+
+namespace rpg_jit {
+
+struct Module {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t search = nullptr;
+  cudaKernel_t evaluate = nullptr;
+  size_t cubin_bytes = 0;
+};
+
+// CUDA source of the specialized kernels for a plan's model.
+std::string generate_source(const rpg::Params& P, const std::vector<double>& coef,
+                            const std::vector<uint64_t>& exps, bool fast);
+
+// NVRTC -> sm_100a cubin.
+int compile(const std::string& source, int min_blocks, std::vector<char>* cubin,
+            std::string* log);
+
+// Generates, compiles (cached per process by source) and loads.
+int get_module(const rpg::Params& P, const std::vector<double>& coef,
+               const std::vector<uint64_t>& exps, bool fast, int device, int min_blocks,
+               Module* out, std::string* err);
+
+}  // namespace rpg_jit

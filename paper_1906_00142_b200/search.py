@@ -32,6 +32,7 @@ class SearchOptions:
     rep_mode: str = "real"          # real | ceil
     tie_rel_tol: float = 1e-12
     arith: str = "exact"            # exact | fast
+    kernel: str = "specialized"     # specialized (per-model NVRTC kernel) | generic
     device: int = 0
 
     def struct(self) -> A.rpg_options:
@@ -39,10 +40,13 @@ class SearchOptions:
             raise ValueError("rep_mode must be real or ceil")
         if self.arith not in ("exact", "fast"):
             raise ValueError("arith must be exact or fast")
+        if self.kernel not in ("specialized", "generic"):
+            raise ValueError("kernel must be specialized or generic")
         return A.options_struct(
             A.RPG_REP_CEIL if self.rep_mode == "ceil" else A.RPG_REP_REAL,
             A.RPG_ARITH_FAST if self.arith == "fast" else A.RPG_ARITH_EXACT,
-            self.tie_rel_tol, self.regs_per_thread, self.shared_words_per_block)
+            self.tie_rel_tol, self.regs_per_thread, self.shared_words_per_block,
+            A.RPG_KERNEL_GENERIC if self.kernel == "generic" else A.RPG_KERNEL_SPECIALIZED)
 
 
 @dataclass

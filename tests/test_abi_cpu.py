@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "rpg.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(rpg_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(rpg_\w+)\s*\(", text, re.M)))
 
 
 def test_library_loads_and_exports_every_declared_symbol():
@@ -33,7 +33,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(A.rpg_winner) == 48
     assert C.sizeof(A.rpg_poly) == 24
     assert C.sizeof(A.rpg_metric) == 16 + 2 * 24
-    assert C.sizeof(A.rpg_options) == 32
+    assert C.sizeof(A.rpg_options) == 40
 
 
 def test_plan_create_rejects_bad_inputs_before_touching_the_device():
@@ -136,3 +136,24 @@ def test_models_json_roundtrip():
         F.parse_models('{"schema":"other-v9"}')
     with pytest.raises(F.PipelineError, match="metrics"):
         F.parse_models('{"schema":"ratprog-models-v1","variables":["D1","bx","by"]}')
+
+
+@pytest.mark.parametrize("arith", [A.RPG_ARITH_EXACT, A.RPG_ARITH_FAST])
+def test_specialized_kernel_source_compiles_for_sm100a(arith):
+    """The per-model kernel source (rpg_emit_cuda_source) compiles with NVRTC
+    for sm_100a on the CPU-only host (no device needed)."""
+    lib = A.load_library()
+    spec = F.models_to_metric_spec(F.read_models(os.path.join(ROOT, "data", "polybench", "2dconv.models.json")))
+    pk = A.PackedModel(spec)
+    hw = A.profile_struct(F.load_profile(os.path.join(ROOT, "data", "b200.profile")))
+    opts = A.options_struct(arith=arith)
+    buf = C.create_string_buffer(1 << 20)
+    err = C.create_string_buffer(4096)
+    cubin = C.c_int64(0)
+    n = lib.rpg_emit_cuda_source(C.byref(pk.struct), C.byref(hw), C.byref(opts), 1, buf, len(buf),
+                                 C.byref(cubin), err, len(err))
+    assert n > 0, err.value
+    src = buf.value.decode()
+    assert "rpg_jit_search" in src and "rpg_jit_evaluate" in src
+    assert ("fma(" in src) == (arith == A.RPG_ARITH_FAST)
+    assert cubin.value > 10000

@@ -23,10 +23,10 @@ CASES = zoo.cases(small=True)
 IDS = [c.name for c in CASES]
 
 
-def _opts(c, arith):
+def _opts(c, arith, kernel="specialized"):
     return S.SearchOptions(regs_per_thread=c.regs_fallback,
                            shared_words_per_block=c.shared_fallback,
-                           rep_mode=c.rep_mode, arith=arith)
+                           rep_mode=c.rep_mode, arith=arith, kernel=kernel)
 
 
 def _oracle(c, arith, what):
@@ -39,10 +39,11 @@ def _oracle(c, arith, what):
     return o1.search_batch(pk, hw, opts, space, c.data, 8)
 
 
+@pytest.mark.parametrize("kernel", ["specialized", "generic"])
 @pytest.mark.parametrize("arith", ["exact", "fast"])
 @pytest.mark.parametrize("case", CASES, ids=IDS)
-def test_evaluate_bit_exact(case, arith):
-    with S.Plan(case.spec, case.hw, case.space, _opts(case, arith)) as plan:
+def test_evaluate_bit_exact(case, arith, kernel):
+    with S.Plan(case.spec, case.hw, case.space, _opts(case, arith, kernel)) as plan:
         ec, tag, wocc = plan.evaluate(case.data)
     oec, otag, owocc = _oracle(case, arith, "evaluate")
     assert np.array_equal(ec.view(np.int64), oec.view(np.int64)) or np.array_equal(ec, oec), (
@@ -51,10 +52,11 @@ def test_evaluate_bit_exact(case, arith):
     assert np.array_equal(wocc, owocc)
 
 
+@pytest.mark.parametrize("kernel", ["specialized", "generic"])
 @pytest.mark.parametrize("arith", ["exact", "fast"])
 @pytest.mark.parametrize("case", CASES, ids=IDS)
-def test_search_winners_bit_exact(case, arith):
-    with S.Plan(case.spec, case.hw, case.space, _opts(case, arith)) as plan:
+def test_search_winners_bit_exact(case, arith, kernel):
+    with S.Plan(case.spec, case.hw, case.space, _opts(case, arith, kernel)) as plan:
         got = plan.search_batch(case.data)
     want = _oracle(case, arith, "search")
     for f in ("cfg_idx", "ties", "n_feasible", "b_active", "w_active", "w_occ", "case_tag"):
@@ -129,15 +131,15 @@ def test_no_feasible_config_flag():
         S.search_optimal(spec, [64], zoo.sample_hw(), F.enumerate_configs())
 
 
-def test_large_space_global_scratch_path():
-    """30,343-config 3-D space: Ec does not fit SMEM and goes through the
-    per-CTA global scratch slices."""
+@pytest.mark.parametrize("kernel", ["specialized", "generic"])
+def test_large_space_3d(kernel):
+    """The full 30,343-config 3-D space (C5 shape)."""
     rng = np.random.default_rng(7)
     spec = zoo.random_spec(rng, ["D1", "D2", "bx", "by", "bz"], sparsity=0.5)
     space = F.integer_configs(dims=3)
     data = rng.integers(16, 2049, size=(6, 2))
     c = zoo.Case("big3d", spec, zoo.b200_hw(), space, data)
-    with S.Plan(spec, c.hw, space, _opts(c, "exact")) as plan:
+    with S.Plan(spec, c.hw, space, _opts(c, "exact", kernel)) as plan:
         got = plan.search_batch(data)
     want = _oracle(c, "exact", "search")
     assert np.array_equal(got, want)
