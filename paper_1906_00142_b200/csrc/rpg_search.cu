@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -259,6 +260,8 @@ int prepare_model(const rpg_model* model, const rpg_profile* hw, const rpg_optio
     pd.s0 = maxd[0] + 1;
     pd.s1 = P.n_cfg_vars > 1 ? maxd[1] + 1 : 1;
     pd.s2 = P.n_cfg_vars > 2 ? maxd[2] + 1 : 1;
+    // Even slot offsets: the specialized kernels read slot pairs (LDS.128).
+    if ((slot_begin.size() - 1) % 2) slot_begin.push_back((int32_t)slot_terms.size());
     pd.slot_off = (int32_t)slot_begin.size() - 1;
     const int n = pd.s0 * pd.s1 * pd.s2;
     if (pd.slot_off + n > 8192)
@@ -293,6 +296,7 @@ int prepare_model(const rpg_model* model, const rpg_profile* hw, const rpg_optio
     for (int v = 0; one && v < nv; ++v) one = m.den.exps[v] == 0;
     md.den_is_one = one ? 1 : 0;
   }
+  if ((slot_begin.size() - 1) % 2) slot_begin.push_back((int32_t)slot_terms.size());
   P.n_terms = (int32_t)coef.size();
   P.n_slots = (int32_t)slot_begin.size() - 1;
   P.occ_const = P.metric[RPG_METRIC_REGS].is_const && P.metric[RPG_METRIC_SHARED].is_const;
@@ -426,7 +430,11 @@ int rpg_plan_create(const rpg_model* model, const rpg_profile* hw, const rpg_con
     return fail(set_err(err, errlen, RPG_E_MODEL, "model too large for shared memory"));
   if (plan->specialized) {
     std::string jerr;
-    if (rpg_jit::get_module(P, coef, exps, plan->fast, device, 3, &plan->jit, &jerr) != 0)
+    // Resident CTAs per SM the specialized kernels are register-budgeted for
+    // (launch bounds); RPG_JIT_MIN_BLOCKS overrides it for tuning sweeps.
+    int min_blocks = 3;
+    if (const char* e = getenv("RPG_JIT_MIN_BLOCKS")) min_blocks = std::max(1, atoi(e));
+    if (rpg_jit::get_module(P, coef, exps, plan->fast, device, min_blocks, &plan->jit, &jerr) != 0)
       return fail(set_err(err, errlen, RPG_E_CUDA, "%s", jerr.c_str()));
   }
   auto setup = [&](const void* fn, int* grid) -> cudaError_t {
