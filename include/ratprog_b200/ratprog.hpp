@@ -1,0 +1,951 @@
+// ratprog_b200/ratprog.hpp — C++17 drop-in for the reference `ratprog` hot
+// path, running on the B200 evaluator behind include/rpg.h (librpgpu.so).
+//
+// Same namespaces, type names, function names, argument meanings and
+// exception types/messages as the reference headers for the search path
+// (citations relative to /root/reference/proj/include/ratprog):
+//   perf::DeviceProfile / parse_profile / load_profile   perfmodel.hpp:50-208
+//   perf::LaunchConfig, RepMode, CaseTag, MetricSpec,
+//   check_metric_spec                                     perfmodel.hpp:79-84, 271-282, 401-456
+//   poly::DegreeBounds / monomial_basis / Polynomial /
+//   RationalFunction                                      polyfit.hpp:41-84
+//   data::enumerate_configs                               datakit.hpp:79-94
+//   pipe::MetricModelSet / parse_models / read_models /
+//   to_metric_spec / generate_rp                          pipeline.hpp:58-68, 188-255, 1020-1089
+//   pipe::SearchOptions / SearchRow / SearchResult /
+//   search_optimal                                        pipeline.hpp:438-680
+//   pipe::format_search_{csv,text,jsonl}                  pipeline.hpp:897-934
+// A caller of the reference's `--models` search path (ratprog_cli.cpp:
+// 277-332) compiles against this header unchanged: `generate_rp` returns an
+// ir::RationalProgram that carries the metric spec, and `search_optimal`
+// evaluates it on the GPU.  New: `search_optimal_batch` sweeps many data
+// tuples per launch.  Every number is computed by librpgpu.so; there is no
+// CPU evaluator here.
+#pragma once
+
+#include <algorithm>
+#include <charconv>
+#include <cmath>
+#include <cstdint>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rpg.h"
+
+namespace ratprog {
+
+// ---------------------------------------------------------------------------
+namespace poly {
+
+struct DimensionMismatch : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DenominatorNearZero : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct DegreeBounds {
+  std::vector<int> num, den;
+};
+
+// Graded-lex exponent tuples (polyfit.hpp:50-73).
+inline std::vector<std::vector<int>> monomial_basis(const std::vector<int>& bounds) {
+  for (int b : bounds)
+    if (b < 0) throw std::invalid_argument("negative degree bound");
+  std::vector<std::vector<int>> tuples{{}};
+  for (int b : bounds) {
+    std::vector<std::vector<int>> next;
+    next.reserve(tuples.size() * (b + 1));
+    for (const auto& t : tuples)
+      for (int e = 0; e <= b; ++e) {
+        next.push_back(t);
+        next.back().push_back(e);
+      }
+    tuples = std::move(next);
+  }
+  std::stable_sort(tuples.begin(), tuples.end(),
+                   [](const std::vector<int>& a, const std::vector<int>& b) {
+                     const int ga = std::accumulate(a.begin(), a.end(), 0);
+                     const int gb = std::accumulate(b.begin(), b.end(), 0);
+                     if (ga != gb) return ga < gb;
+                     return a < b;
+                   });
+  return tuples;
+}
+
+struct Polynomial {
+  std::vector<std::string> variables;
+  std::vector<std::vector<int>> basis;
+  std::vector<double> coeffs;
+};
+
+struct RationalFunction {
+  Polynomial num, den;
+};
+
+struct FitReport {
+  double residual_norm = 0.0;
+  int numerical_rank = 0;
+  std::vector<double> singular_values;
+  bool truncated = false;
+};
+
+}  // namespace poly
+
+// ---------------------------------------------------------------------------
+namespace perf {
+
+struct ProfileError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ModelError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct DeviceProfile {
+  long long R_max = 0, Z_max = 0, T_max = 0, B_max = 0, W_max = 0, num_SM = 0;
+  double freq_GHz = 0, mem_latency_cycles = 0, departure_del_coal_cycles = 0,
+         departure_del_uncoal_cycles = 0, mem_bandwidth_GBps = 0, issue_cycles = 0;
+  long long load_bytes_per_warp = 0, uncoal_per_mw = 0;
+};
+
+struct LaunchConfig {
+  long long bx = 1, by = 1, bz = 1;
+  long long threads() const { return bx * by * bz; }
+  bool operator==(const LaunchConfig& o) const { return bx == o.bx && by == o.by && bz == o.bz; }
+  bool operator<(const LaunchConfig& o) const {
+    if (bx != o.bx) return bx < o.bx;
+    if (by != o.by) return by < o.by;
+    return bz < o.bz;
+  }
+};
+
+enum class RepMode { Real, Ceil };
+enum class CaseTag { BothSaturated, CwpBound, MwpBound };
+
+inline const char* case_name(CaseTag t) {
+  switch (t) {
+    case CaseTag::BothSaturated: return "both_saturated";
+    case CaseTag::CwpBound: return "cwp_bound";
+    case CaseTag::MwpBound: return "mwp_bound";
+  }
+  return "?";
+}
+
+namespace detail {
+inline const std::vector<std::string>& profile_keys() {
+  static const std::vector<std::string> keys = {
+      "R_max", "Z_max", "T_max", "B_max", "W_max", "num_SM", "freq_GHz",
+      "mem_latency_cycles", "departure_del_coal_cycles", "departure_del_uncoal_cycles",
+      "mem_bandwidth_GBps", "issue_cycles", "load_bytes_per_warp", "uncoal_per_mw"};
+  return keys;
+}
+inline std::string trim(const std::string& s) {
+  const size_t b = s.find_first_not_of(" \t\r");
+  const size_t e = s.find_last_not_of(" \t\r");
+  return b == std::string::npos ? std::string() : s.substr(b, e - b + 1);
+}
+}  // namespace detail
+
+// perf::parse_profile (perfmodel.hpp:111-180): same checks and messages.
+inline DeviceProfile parse_profile(const std::string& text) {
+  std::map<std::string, double> seen;
+  std::istringstream in(text);
+  std::string line;
+  size_t line_no = 0;
+  const auto& keys = detail::profile_keys();
+  while (std::getline(in, line)) {
+    ++line_no;
+    const std::string stripped = line.substr(0, line.find('#'));
+    if (stripped.find_first_not_of(" \t\r") == std::string::npos) continue;
+    const size_t eq = stripped.find('=');
+    if (eq == std::string::npos)
+      throw ProfileError("profile line " + std::to_string(line_no) + ": expected 'key = value'");
+    const std::string key = detail::trim(stripped.substr(0, eq));
+    const std::string value = detail::trim(stripped.substr(eq + 1));
+    if (std::find(keys.begin(), keys.end(), key) == keys.end())
+      throw ProfileError("profile line " + std::to_string(line_no) + ": unknown key '" + key + "'");
+    if (seen.count(key))
+      throw ProfileError("profile line " + std::to_string(line_no) + ": duplicate key '" + key + "'");
+    double v = 0;
+    try {
+      size_t used = 0;
+      v = std::stod(value, &used);
+      if (used != value.size()) throw std::invalid_argument(value);
+    } catch (const std::exception&) {
+      throw ProfileError("profile line " + std::to_string(line_no) + ": bad numeric value '" +
+                         value + "'");
+    }
+    if (!(v > 0))
+      throw ProfileError("profile line " + std::to_string(line_no) + ": '" + key +
+                         "' must be positive");
+    seen[key] = v;
+  }
+  for (const std::string& key : keys)
+    if (!seen.count(key)) throw ProfileError("profile is missing key '" + key + "'");
+  auto as_count = [&](const std::string& key) {
+    const double v = seen[key];
+    if (v != std::floor(v)) throw ProfileError("profile key '" + key + "' must be an integer");
+    return static_cast<long long>(v);
+  };
+  DeviceProfile hw;
+  hw.R_max = as_count("R_max");
+  hw.Z_max = as_count("Z_max");
+  hw.T_max = as_count("T_max");
+  hw.B_max = as_count("B_max");
+  hw.W_max = as_count("W_max");
+  hw.num_SM = as_count("num_SM");
+  hw.freq_GHz = seen["freq_GHz"];
+  hw.mem_latency_cycles = seen["mem_latency_cycles"];
+  hw.departure_del_coal_cycles = seen["departure_del_coal_cycles"];
+  hw.departure_del_uncoal_cycles = seen["departure_del_uncoal_cycles"];
+  hw.mem_bandwidth_GBps = seen["mem_bandwidth_GBps"];
+  hw.issue_cycles = seen["issue_cycles"];
+  hw.load_bytes_per_warp = as_count("load_bytes_per_warp");
+  hw.uncoal_per_mw = as_count("uncoal_per_mw");
+  if (hw.T_max > 1024) throw ProfileError("T_max exceeds 1024, the architectural block limit");
+  return hw;
+}
+
+inline DeviceProfile load_profile(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw ProfileError("cannot open device profile '" + path + "'");
+  std::ostringstream buf;
+  buf << in.rdbuf();
+  try {
+    return parse_profile(buf.str());
+  } catch (const ProfileError& e) {
+    throw ProfileError(path + ": " + e.what());
+  }
+}
+
+inline constexpr const char* kMetricComp = "comp_insts_per_thread";
+inline constexpr const char* kMetricUncoal = "uncoal_mem_insts_per_thread";
+inline constexpr const char* kMetricCoal = "coal_mem_insts_per_thread";
+inline constexpr const char* kMetricSynch = "synch_insts_per_block";
+inline constexpr const char* kMetricTotalBlocks = "total_blocks";
+inline constexpr const char* kMetricRegs = "regs_per_thread";
+inline constexpr const char* kMetricShared = "shared_words_per_block";
+
+inline const std::vector<std::string>& required_metric_names() {
+  static const std::vector<std::string> names = {kMetricComp, kMetricUncoal, kMetricCoal,
+                                                 kMetricSynch, kMetricTotalBlocks};
+  return names;
+}
+
+struct MetricSpec {
+  std::vector<std::string> variables;
+  std::map<std::string, poly::RationalFunction> models;
+  std::map<std::string, double> constants;
+  bool covers(const std::string& name) const {
+    return models.count(name) || constants.count(name);
+  }
+};
+
+// perf::check_metric_spec (perfmodel.hpp:428-456).
+inline void check_metric_spec(const MetricSpec& spec) {
+  for (const std::string& name : required_metric_names())
+    if (!spec.covers(name))
+      throw ModelError("metric '" + name + "' has neither a model nor a constant");
+  for (const char* name : {kMetricRegs, kMetricShared})
+    if (!spec.covers(name))
+      throw ModelError(std::string("metric '") + name + "' has neither a model nor a constant");
+  bool has_bx = false, has_by = false;
+  for (const std::string& v : spec.variables) {
+    has_bx |= v == "bx";
+    has_by |= v == "by";
+    const auto& hw_keys = detail::profile_keys();
+    if (std::find(hw_keys.begin(), hw_keys.end(), v) != hw_keys.end())
+      throw ModelError("variable '" + v + "' collides with a hardware field");
+    const bool data_param = v.size() >= 2 && v[0] == 'D' &&
+                            v.find_first_not_of("0123456789", 1) == std::string::npos;
+    if (!data_param && v != "bx" && v != "by" && v != "bz")
+      throw ModelError("variable '" + v + "' is not a data parameter (D1..Dd) or block dimension");
+  }
+  if (!has_bx || !has_by) throw ModelError("metric variables must include bx and by");
+  for (const auto& [name, f] : spec.models)
+    if (f.num.variables != spec.variables)
+      throw ModelError("model '" + name + "' disagrees with the shared variable order");
+}
+
+struct EmitOptions {
+  RepMode rep_mode = RepMode::Real;
+  int scale_pow10 = 40;
+};
+
+}  // namespace perf
+
+// ---------------------------------------------------------------------------
+namespace data {
+
+// data::enumerate_configs (datakit.hpp:79-94).
+inline std::vector<perf::LaunchConfig> enumerate_configs(long long max_threads = 1024,
+                                                         long long min_threads = 32,
+                                                         int dims = 2) {
+  if (min_threads < 1 || min_threads > max_threads || max_threads > 1024)
+    throw std::invalid_argument("enumerate_configs: need 1 <= min_threads <= max_threads <= 1024");
+  if (dims < 1 || dims > 3) throw std::invalid_argument("enumerate_configs: dims must be 1, 2 or 3");
+  std::vector<perf::LaunchConfig> out;
+  for (long long bx = 1; bx <= 1024; bx *= 2)
+    for (long long by = 1; by <= (dims >= 2 ? 1024 : 1); by *= 2)
+      for (long long bz = 1; bz <= (dims >= 3 ? 1024 : 1); bz *= 2) {
+        const long long t = bx * by * bz;
+        if (t >= min_threads && t <= max_threads) out.push_back({bx, by, bz});
+      }
+  return out;
+}
+
+// Every integer block shape with min <= bx*by[*bz] <= max (the dense grids
+// of the benchmark sweeps; lex order).
+inline std::vector<perf::LaunchConfig> integer_configs(long long max_threads = 1024, int dims = 2,
+                                                       long long min_threads = 1) {
+  std::vector<perf::LaunchConfig> out;
+  for (long long bx = 1; bx <= max_threads; ++bx)
+    for (long long by = 1; by <= (dims >= 2 ? max_threads / bx : 1); ++by)
+      for (long long bz = 1; bz <= (dims >= 3 ? max_threads / (bx * by) : 1); ++bz)
+        if (bx * by * bz >= min_threads) out.push_back({bx, by, bz});
+  return out;
+}
+
+}  // namespace data
+
+// ---------------------------------------------------------------------------
+// Minimal JSON reader for the models / kernel-spec files.
+namespace json {
+
+struct Value {
+  enum Kind { Null, Bool, Number, String, Array, Object } kind = Null;
+  bool b = false;
+  double num = 0;
+  std::string str;
+  std::vector<Value> arr;
+  std::vector<std::pair<std::string, Value>> obj;
+  const Value* find(const std::string& k) const {
+    for (const auto& kv : obj)
+      if (kv.first == k) return &kv.second;
+    return nullptr;
+  }
+};
+
+struct ParseError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+class Parser {
+ public:
+  explicit Parser(const std::string& s) : s_(s) {}
+  Value parse() {
+    Value v = value();
+    ws();
+    if (i_ != s_.size()) fail("trailing characters");
+    return v;
+  }
+
+ private:
+  const std::string& s_;
+  size_t i_ = 0;
+  [[noreturn]] void fail(const char* why) {
+    throw ParseError(std::string(why) + " at offset " + std::to_string(i_));
+  }
+  void ws() {
+    while (i_ < s_.size() && (s_[i_] == ' ' || s_[i_] == '\n' || s_[i_] == '\t' || s_[i_] == '\r')) ++i_;
+  }
+  Value value() {
+    ws();
+    if (i_ >= s_.size()) fail("unexpected end");
+    const char c = s_[i_];
+    Value v;
+    if (c == '{') {
+      v.kind = Value::Object;
+      ++i_;
+      ws();
+      if (i_ < s_.size() && s_[i_] == '}') { ++i_; return v; }
+      while (true) {
+        ws();
+        if (i_ >= s_.size() || s_[i_] != '"') fail("expected key");
+        std::string k = string();
+        ws();
+        if (i_ >= s_.size() || s_[i_] != ':') fail("expected ':'");
+        ++i_;
+        v.obj.emplace_back(std::move(k), value());
+        ws();
+        if (i_ < s_.size() && s_[i_] == ',') { ++i_; continue; }
+        if (i_ < s_.size() && s_[i_] == '}') { ++i_; break; }
+        fail("expected ',' or '}'");
+      }
+    } else if (c == '[') {
+      v.kind = Value::Array;
+      ++i_;
+      ws();
+      if (i_ < s_.size() && s_[i_] == ']') { ++i_; return v; }
+      while (true) {
+        v.arr.push_back(value());
+        ws();
+        if (i_ < s_.size() && s_[i_] == ',') { ++i_; continue; }
+        if (i_ < s_.size() && s_[i_] == ']') { ++i_; break; }
+        fail("expected ',' or ']'");
+      }
+    } else if (c == '"') {
+      v.kind = Value::String;
+      v.str = string();
+    } else if (s_.compare(i_, 4, "true") == 0) {
+      v.kind = Value::Bool; v.b = true; i_ += 4;
+    } else if (s_.compare(i_, 5, "false") == 0) {
+      v.kind = Value::Bool; i_ += 5;
+    } else if (s_.compare(i_, 4, "null") == 0) {
+      i_ += 4;
+    } else {
+      v.kind = Value::Number;
+      const char* b = s_.c_str() + i_;
+      char* e = nullptr;
+      v.num = std::strtod(b, &e);
+      if (e == b) fail("bad value");
+      i_ += static_cast<size_t>(e - b);
+    }
+    return v;
+  }
+  std::string string() {
+    ++i_;  // opening quote
+    std::string out;
+    while (i_ < s_.size() && s_[i_] != '"') {
+      if (s_[i_] == '\\') {
+        ++i_;
+        if (i_ >= s_.size()) fail("bad escape");
+        const char e = s_[i_];
+        out += e == 'n' ? '\n' : e == 't' ? '\t' : e == 'r' ? '\r' : e;
+      } else {
+        out += s_[i_];
+      }
+      ++i_;
+    }
+    if (i_ >= s_.size()) fail("unterminated string");
+    ++i_;
+    return out;
+  }
+};
+
+inline Value parse(const std::string& text) { return Parser(text).parse(); }
+
+}  // namespace json
+
+// ---------------------------------------------------------------------------
+namespace pipe {
+
+struct PipelineError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NoFeasibleConfig : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct MetricModel {
+  poly::RationalFunction fn;
+  poly::FitReport report;
+};
+
+struct MetricModelSet {
+  std::vector<std::string> variables;
+  std::map<std::string, MetricModel> models;
+  std::map<std::string, double> constants;
+  std::map<std::string, std::string> failures;
+};
+
+namespace detail {
+
+inline std::vector<int> int_array(const json::Value& v, const std::string& what) {
+  if (v.kind != json::Value::Array) throw PipelineError(what + " must be an array");
+  std::vector<int> out;
+  for (const auto& x : v.arr) out.push_back(static_cast<int>(x.num));
+  return out;
+}
+
+inline std::vector<double> num_array(const json::Value& v, const std::string& what) {
+  if (v.kind != json::Value::Array) throw PipelineError(what + " must be an array");
+  std::vector<double> out;
+  for (const auto& x : v.arr) out.push_back(x.num);
+  return out;
+}
+
+// datakit.hpp:491-517 (ratfunc_from_json): same messages.
+inline poly::RationalFunction ratfunc_from_json(const json::Value& j,
+                                                const std::vector<std::string>& variables,
+                                                const std::string& metric) {
+  for (const char* key : {"num_bounds", "num_coeffs", "den_bounds", "den_coeffs"})
+    if (!j.find(key))
+      throw PipelineError("metric '" + metric + "' is missing '" + key + "'");
+  poly::RationalFunction f;
+  auto read_poly = [&](const char* bkey, const char* ckey, poly::Polynomial& p) {
+    const std::vector<int> bounds = int_array(*j.find(bkey), bkey);
+    if (bounds.size() != variables.size())
+      throw PipelineError("metric '" + metric + "': '" + bkey + "' must have one entry per variable");
+    p.variables = variables;
+    p.basis = poly::monomial_basis(bounds);
+    p.coeffs = num_array(*j.find(ckey), ckey);
+    if (p.coeffs.size() != p.basis.size())
+      throw PipelineError("metric '" + metric + "': '" + std::string(ckey) + "' must have " +
+                          std::to_string(p.basis.size()) + " entries for these bounds");
+  };
+  read_poly("num_bounds", "num_coeffs", f.num);
+  read_poly("den_bounds", "den_coeffs", f.den);
+  return f;
+}
+
+}  // namespace detail
+
+// pipe::parse_models (pipeline.hpp:1020-1069).
+inline MetricModelSet parse_models(const std::string& text) {
+  json::Value j;
+  try {
+    j = json::parse(text);
+  } catch (const json::ParseError& e) {
+    throw PipelineError(std::string("models file is not valid JSON: ") + e.what());
+  }
+  const json::Value* schema = j.find("schema");
+  if (!schema || schema->str != "ratprog-models-v1")
+    throw PipelineError("models file schema must be 'ratprog-models-v1'");
+  MetricModelSet m;
+  const json::Value* vars = j.find("variables");
+  if (!vars) throw PipelineError("models file is malformed: missing 'variables'");
+  for (const auto& v : vars->arr) m.variables.push_back(v.str);
+  if (m.variables.empty()) throw PipelineError("models file declares no variables");
+  if (const json::Value* c = j.find("constants"))
+    for (const auto& kv : c->obj) m.constants[kv.first] = kv.second.num;
+  const json::Value* metrics = j.find("metrics");
+  if (!metrics || metrics->kind != json::Value::Object)
+    throw PipelineError("models file is missing the 'metrics' object");
+  for (const auto& [name, body] : metrics->obj) {
+    MetricModel model;
+    model.fn = detail::ratfunc_from_json(body, m.variables, name);
+    if (const json::Value* rep = body.find("report")) {
+      if (const json::Value* r = rep->find("residual_norm")) model.report.residual_norm = r->num;
+      if (const json::Value* r = rep->find("numerical_rank"))
+        model.report.numerical_rank = static_cast<int>(r->num);
+      if (const json::Value* r = rep->find("truncated")) model.report.truncated = r->b;
+    }
+    m.models[name] = std::move(model);
+  }
+  if (const json::Value* f = j.find("failures"))
+    for (const auto& kv : f->obj) m.failures[kv.first] = kv.second.str;
+  return m;
+}
+
+inline MetricModelSet read_models(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw PipelineError("cannot open '" + path + "' for reading");
+  std::ostringstream buf;
+  buf << in.rdbuf();
+  try {
+    return parse_models(buf.str());
+  } catch (const PipelineError& e) {
+    throw PipelineError(path + ": " + e.what());
+  }
+}
+
+// pipe::to_metric_spec (pipeline.hpp:188-195).
+inline perf::MetricSpec to_metric_spec(const MetricModelSet& m) {
+  perf::MetricSpec spec;
+  spec.variables = m.variables;
+  for (const auto& [name, model] : m.models) spec.models[name] = model.fn;
+  spec.constants = m.constants;
+  perf::check_metric_spec(spec);
+  return spec;
+}
+
+}  // namespace pipe
+
+// The reference's rational program (ir.hpp:19-112) is, on this path, the
+// emitted MWP-CWP program of a metric spec with a profile baked in
+// (pipeline.hpp:233-255).  The B200 build evaluates that program's
+// semantics directly, so the program object carries its spec.
+namespace ir {
+struct RationalProgram {
+  std::shared_ptr<const perf::MetricSpec> spec;
+  perf::RepMode rep_mode = perf::RepMode::Real;
+  std::vector<std::string> inputs;
+  std::string output = "total_cycles";
+};
+}  // namespace ir
+
+namespace pipe {
+
+inline ir::RationalProgram generate_rp(const MetricModelSet& models, const perf::DeviceProfile&,
+                                       const perf::EmitOptions& opts = {}) {
+  ir::RationalProgram rp;
+  rp.spec = std::make_shared<perf::MetricSpec>(to_metric_spec(models));
+  rp.rep_mode = opts.rep_mode;
+  rp.inputs = rp.spec->variables;
+  return rp;
+}
+
+enum class Arith { Exact, Fast };
+enum class Kernel { Specialized, Generic };
+
+// pipe::SearchOptions (pipeline.hpp:438-452) + B200 knobs.
+struct SearchOptions {
+  double regs_per_thread = 0.0;
+  double shared_words_per_block = 0.0;
+  const perf::MetricSpec* metrics = nullptr;
+  perf::RepMode rep_mode = perf::RepMode::Real;
+  int jobs = 1;  // accepted for source compatibility; the GPU needs no host threads
+  double tie_rel_tol = 1e-12;
+  std::size_t step_limit = 1000000;  // accepted for source compatibility
+  Arith arith = Arith::Exact;
+  Kernel kernel = Kernel::Specialized;
+  int device = 0;
+};
+
+struct SearchRow {
+  perf::LaunchConfig config;
+  double estimated_cycles = 0.0;
+  double occupancy = 0.0;
+  std::string case_tag = "-";
+};
+
+struct SearchResult {
+  std::vector<SearchRow> ranking;
+  std::size_t ties = 1;
+  std::size_t evaluated = 0;
+  std::size_t infeasible = 0;
+  const SearchRow& best() const { return ranking.front(); }
+};
+
+// Per-data-tuple winner of search_optimal_batch (rpg_winner).
+struct Winner {
+  perf::LaunchConfig config;
+  long long cfg_index = -1;  // -1: no feasible configuration
+  double estimated_cycles = 0.0;
+  double best_cycles = 0.0;
+  double occupancy = 0.0;
+  std::string case_tag = "-";
+  std::size_t ties = 0;
+  std::size_t feasible = 0;
+  long long b_active = 0, w_active = 0;
+};
+
+namespace detail {
+
+inline int rpg_kind(const std::string& v) {
+  if (v == "bx") return RPG_VAR_BX;
+  if (v == "by") return RPG_VAR_BY;
+  if (v == "bz") return RPG_VAR_BZ;
+  return std::stoi(v.substr(1)) - 1;
+}
+
+inline void rethrow(int code, const char* err) {
+  const std::string msg(err);
+  switch (code) {
+    case RPG_E_INVALID: throw std::invalid_argument(msg);
+    case RPG_E_MODEL: throw perf::ModelError(msg);
+    case RPG_E_PROFILE: throw perf::ProfileError(msg);
+    case RPG_E_PIPELINE: throw PipelineError(msg);
+    case RPG_E_NO_FEASIBLE: throw NoFeasibleConfig(msg);
+    default: throw std::runtime_error("librpgpu: " + msg);
+  }
+}
+
+// Owns the packed (AltArr-like) term tables an rpg_model points into.
+struct PackedModel {
+  rpg_model model{};
+  std::vector<std::vector<double>> coefs;
+  std::vector<std::vector<uint8_t>> exps;
+
+  explicit PackedModel(const perf::MetricSpec& spec) {
+    perf::check_metric_spec(spec);
+    const size_t nv = spec.variables.size();
+    if (nv > RPG_MAX_VARS) throw perf::ModelError("too many model variables");
+    model.n_vars = static_cast<int32_t>(nv);
+    for (size_t i = 0; i < nv; ++i) model.var_kind[i] = rpg_kind(spec.variables[i]);
+    const char* slots[RPG_N_METRICS] = {perf::kMetricRegs, perf::kMetricShared,
+                                        perf::kMetricComp, perf::kMetricUncoal,
+                                        perf::kMetricCoal, perf::kMetricSynch,
+                                        perf::kMetricTotalBlocks};
+    coefs.reserve(2 * RPG_N_METRICS);
+    exps.reserve(2 * RPG_N_METRICS);
+    for (int s = 0; s < RPG_N_METRICS; ++s) {
+      rpg_metric& m = model.metric[s];
+      auto c = spec.constants.find(slots[s]);
+      if (c != spec.constants.end()) {  // constants take priority (perfmodel.hpp:463-465)
+        m.is_const = 1;
+        m.value = c->second;
+        continue;
+      }
+      const poly::RationalFunction& f = spec.models.at(slots[s]);
+      m.num = pack(f.num, nv);
+      m.den = pack(f.den, nv);
+    }
+  }
+
+  rpg_poly pack(const poly::Polynomial& p, size_t nv) {
+    std::vector<double> c;
+    std::vector<uint8_t> e;
+    for (size_t k = 0; k < p.coeffs.size(); ++k) {
+      if (p.coeffs[k] == 0.0) continue;  // emit_ratfunc skips zeros (perfmodel.hpp:521)
+      c.push_back(p.coeffs[k]);
+      for (size_t v = 0; v < nv; ++v) e.push_back(static_cast<uint8_t>(p.basis[k][v]));
+    }
+    coefs.push_back(std::move(c));
+    exps.push_back(std::move(e));
+    rpg_poly out{};
+    out.n_terms = static_cast<int32_t>(coefs.back().size());
+    out.coef = coefs.back().data();
+    out.exps = exps.back().data();
+    return out;
+  }
+};
+
+inline rpg_profile to_rpg(const perf::DeviceProfile& hw) {
+  rpg_profile p;
+  p.R_max = hw.R_max; p.Z_max = hw.Z_max; p.T_max = hw.T_max; p.B_max = hw.B_max;
+  p.W_max = hw.W_max; p.num_SM = hw.num_SM; p.freq_GHz = hw.freq_GHz;
+  p.mem_latency_cycles = hw.mem_latency_cycles;
+  p.departure_del_coal_cycles = hw.departure_del_coal_cycles;
+  p.departure_del_uncoal_cycles = hw.departure_del_uncoal_cycles;
+  p.mem_bandwidth_GBps = hw.mem_bandwidth_GBps; p.issue_cycles = hw.issue_cycles;
+  p.load_bytes_per_warp = hw.load_bytes_per_warp; p.uncoal_per_mw = hw.uncoal_per_mw;
+  return p;
+}
+
+inline rpg_options to_rpg(const SearchOptions& o) {
+  rpg_options r{};
+  r.rep_mode = o.rep_mode == perf::RepMode::Ceil ? RPG_REP_CEIL : RPG_REP_REAL;
+  r.arith = o.arith == Arith::Fast ? RPG_ARITH_FAST : RPG_ARITH_EXACT;
+  r.tie_rel_tol = o.tie_rel_tol;
+  r.regs_per_thread = o.regs_per_thread;
+  r.shared_words_per_block = o.shared_words_per_block;
+  r.kernel = o.kernel == Kernel::Generic ? RPG_KERNEL_GENERIC : RPG_KERNEL_SPECIALIZED;
+  return r;
+}
+
+inline std::string case_label(int tag) {
+  switch (tag) {
+    case RPG_CASE_BOTH_SATURATED: return "both_saturated";
+    case RPG_CASE_CWP_BOUND: return "cwp_bound";
+    case RPG_CASE_MWP_BOUND: return "mwp_bound";
+    default: return "-";
+  }
+}
+
+}  // namespace detail
+
+// A metric spec + profile + configuration space resident on one GPU.
+class Plan {
+ public:
+  Plan(const perf::MetricSpec& spec, const perf::DeviceProfile& hw,
+       const std::vector<perf::LaunchConfig>& space, const SearchOptions& opts = {})
+      : packed_(spec), space_(space), W_max_(hw.W_max) {
+    if (space.empty())
+      throw std::invalid_argument("search_optimal: configuration space is empty");
+    for (const std::string& v : spec.variables)
+      if (v[0] == 'D') d_ = std::max(d_, std::stoi(v.substr(1)));
+    std::vector<rpg_config> cfg(space.size());
+    for (size_t i = 0; i < space.size(); ++i) cfg[i] = {space[i].bx, space[i].by, space[i].bz};
+    const rpg_profile p = detail::to_rpg(hw);
+    const rpg_options o = detail::to_rpg(opts);
+    char err[512] = {0};
+    const int rc = rpg_plan_create(&packed_.model, &p, cfg.data(), (int64_t)cfg.size(), &o,
+                                   opts.device, &plan_, err, sizeof(err));
+    if (rc != RPG_OK) detail::rethrow(rc, err);
+  }
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+  ~Plan() { rpg_plan_destroy(plan_); }
+
+  // Winners for every data tuple (rows of `tuples`, each D1..Dd).
+  std::vector<Winner> search(const std::vector<std::vector<long long>>& tuples) const {
+    const int32_t d = tuples.empty() ? d_ : static_cast<int32_t>(tuples.front().size());
+    std::vector<int64_t> flat;
+    flat.reserve(tuples.size() * d);
+    for (const auto& t : tuples) {
+      if ((int32_t)t.size() != d) throw std::invalid_argument("data tuples differ in arity");
+      flat.insert(flat.end(), t.begin(), t.end());
+    }
+    std::vector<rpg_winner> w(tuples.size());
+    char err[512] = {0};
+    const int rc = rpg_search_batch(plan_, flat.data(), (int64_t)tuples.size(), d, w.data(), err,
+                                    sizeof(err));
+    if (rc != RPG_OK) detail::rethrow(rc, err);
+    std::vector<Winner> out(w.size());
+    for (size_t i = 0; i < w.size(); ++i) {
+      Winner& r = out[i];
+      r.cfg_index = w[i].cfg_idx;
+      r.feasible = (size_t)w[i].n_feasible;
+      if (w[i].cfg_idx < 0) continue;
+      r.config = space_[w[i].cfg_idx];
+      r.estimated_cycles = w[i].ec;
+      r.best_cycles = w[i].best_ec;
+      r.occupancy = (double)w[i].w_occ / (double)W_max_;
+      r.case_tag = detail::case_label(w[i].case_tag);
+      r.ties = (size_t)w[i].ties;
+      r.b_active = w[i].b_active;
+      r.w_active = w[i].w_active;
+    }
+    return out;
+  }
+
+  // Per-config program output / case tag / occupancy warps for one tuple.
+  void evaluate(const std::vector<long long>& tuple, std::vector<double>* ec,
+                std::vector<uint8_t>* tag, std::vector<int32_t>* wocc) const {
+    const size_t n = space_.size();
+    ec->assign(n, 0.0);
+    tag->assign(n, 0);
+    wocc->assign(n, 0);
+    std::vector<int64_t> t(tuple.begin(), tuple.end());
+    char err[512] = {0};
+    const int rc = rpg_evaluate(plan_, t.data(), 1, (int32_t)t.size(), ec->data(), tag->data(),
+                                wocc->data(), err, sizeof(err));
+    if (rc != RPG_OK) detail::rethrow(rc, err);
+  }
+
+  const std::vector<perf::LaunchConfig>& space() const { return space_; }
+  long long W_max() const { return W_max_; }
+
+ private:
+  detail::PackedModel packed_;
+  std::vector<perf::LaunchConfig> space_;
+  long long W_max_;
+  int32_t d_ = 0;
+  rpg_plan* plan_ = nullptr;
+};
+
+// pipe::search_optimal for a metric spec (pipeline.hpp:575-680): the GPU
+// evaluates every configuration; the rows are ordered exactly as the
+// reference orders them (feasible = Ec >= 0; sort by (Ec, lex); tie group
+// Ec <= best + best*tol, stable-sorted by occupancy, descending).
+inline SearchResult search_optimal(const perf::MetricSpec& spec,
+                                   const std::vector<long long>& data_params,
+                                   const perf::DeviceProfile& hw,
+                                   const std::vector<perf::LaunchConfig>& space,
+                                   const SearchOptions& opts = {}) {
+  if (space.empty()) throw std::invalid_argument("search_optimal: configuration space is empty");
+  Plan plan(spec, hw, space, opts);
+  std::vector<double> ec;
+  std::vector<uint8_t> tag;
+  std::vector<int32_t> wocc;
+  plan.evaluate(data_params, &ec, &tag, &wocc);
+  const size_t n = space.size();
+  std::vector<size_t> feasible;
+  for (size_t i = 0; i < n; ++i)
+    if (ec[i] >= 0) feasible.push_back(i);
+  if (feasible.empty())
+    throw NoFeasibleConfig("no configuration in the search space can launch on this device");
+  std::sort(feasible.begin(), feasible.end(), [&](size_t a, size_t b) {
+    if (ec[a] != ec[b]) return ec[a] < ec[b];
+    if (space[a] < space[b]) return true;
+    if (space[b] < space[a]) return false;
+    return a < b;
+  });
+  const double best = ec[feasible.front()];
+  const double bound = best + best * opts.tie_rel_tol;
+  size_t ties = 0;
+  while (ties < feasible.size() && ec[feasible[ties]] <= bound) ++ties;
+  std::stable_sort(feasible.begin(), feasible.begin() + ties,
+                   [&](size_t a, size_t b) { return wocc[a] > wocc[b]; });
+  SearchResult out;
+  out.evaluated = n;
+  out.infeasible = n - feasible.size();
+  out.ties = ties;
+  out.ranking.reserve(feasible.size());
+  for (size_t i : feasible)
+    out.ranking.push_back(SearchRow{space[i], ec[i], (double)wocc[i] / (double)hw.W_max,
+                                    detail::case_label(tag[i])});
+  return out;
+}
+
+// The reference's signature (pipeline.hpp:575-579) for programs produced by
+// generate_rp; occupancy comes from opts.metrics when given (as in the
+// reference), else from the program's own spec.
+inline SearchResult search_optimal(const ir::RationalProgram& rp,
+                                   const std::vector<long long>& data_params,
+                                   const perf::DeviceProfile& hw,
+                                   const std::vector<perf::LaunchConfig>& space,
+                                   const SearchOptions& opts = {}) {
+  if (!rp.spec)
+    throw PipelineError("program was not generated from a metric spec; bare-program search "
+                        "is not supported by the B200 path yet");
+  SearchOptions o = opts;
+  o.rep_mode = rp.rep_mode;
+  return search_optimal(opts.metrics ? *opts.metrics : *rp.spec, data_params, hw, space, o);
+}
+
+// Batched search: one winner per data tuple, all tuples in one launch.
+inline std::vector<Winner> search_optimal_batch(const perf::MetricSpec& spec,
+                                                const std::vector<std::vector<long long>>& tuples,
+                                                const perf::DeviceProfile& hw,
+                                                const std::vector<perf::LaunchConfig>& space,
+                                                const SearchOptions& opts = {}) {
+  Plan plan(spec, hw, space, opts);
+  return plan.search(tuples);
+}
+
+// ---------------------------------------------------------------------------
+// Report formatters (pipeline.hpp:897-934), deterministic.
+
+namespace detail {
+inline std::string format_double(double v) {
+  char buf[64];
+  auto res = std::to_chars(buf, buf + sizeof(buf), v);
+  return std::string(buf, res.ptr);
+}
+inline std::string config_label(const perf::LaunchConfig& c) {
+  return std::to_string(c.bx) + "x" + std::to_string(c.by) + "x" + std::to_string(c.bz);
+}
+}  // namespace detail
+
+inline std::string format_search_csv(const SearchResult& r) {
+  std::ostringstream out;
+  out << "bx,by,bz,Ec,occupancy,case\n";
+  for (const SearchRow& row : r.ranking)
+    out << row.config.bx << "," << row.config.by << "," << row.config.bz << ","
+        << detail::format_double(row.estimated_cycles) << ","
+        << detail::format_double(row.occupancy) << "," << row.case_tag << "\n";
+  return out.str();
+}
+
+inline std::string format_search_text(const SearchResult& r) {
+  std::vector<std::vector<std::string>> rows;
+  for (const SearchRow& row : r.ranking)
+    rows.push_back({detail::config_label(row.config), detail::format_double(row.estimated_cycles),
+                    detail::format_double(row.occupancy), row.case_tag});
+  const std::vector<std::string> header = {"config", "Ec", "occupancy", "case"};
+  std::vector<size_t> width(header.size());
+  for (size_t j = 0; j < header.size(); ++j) width[j] = header[j].size();
+  for (const auto& row : rows)
+    for (size_t j = 0; j < row.size(); ++j) width[j] = std::max(width[j], row[j].size());
+  std::ostringstream out;
+  auto emit = [&](const std::vector<std::string>& row) {
+    for (size_t j = 0; j < row.size(); ++j) {
+      out << row[j];
+      if (j + 1 < row.size()) out << std::string(width[j] - row[j].size() + 2, ' ');
+    }
+    out << "\n";
+  };
+  emit(header);
+  size_t total = 0;
+  for (size_t j = 0; j < width.size(); ++j) total += width[j] + (j + 1 < width.size() ? 2 : 0);
+  out << std::string(total, '-') << "\n";
+  for (const auto& row : rows) emit(row);
+  out << "evaluated " << r.evaluated << " configuration(s), " << r.infeasible
+      << " infeasible; optimum ties: " << r.ties << "\n";
+  return out.str();
+}
+
+inline std::string format_search_jsonl(const SearchResult& r) {
+  std::string out;
+  for (const SearchRow& row : r.ranking) {
+    out += "{\"config\":[" + std::to_string(row.config.bx) + "," + std::to_string(row.config.by) +
+           "," + std::to_string(row.config.bz) + "],\"Ec\":" +
+           detail::format_double(row.estimated_cycles) +
+           ",\"occupancy\":" + detail::format_double(row.occupancy) + ",\"case_tag\":\"" +
+           row.case_tag + "\"}\n";
+  }
+  return out;
+}
+
+}  // namespace pipe
+}  // namespace ratprog
