@@ -98,9 +98,9 @@ int validate_profile(const rpg_profile* hw, char* err, size_t errlen) {
   if (hw->T_max > 1024)
     return set_err(err, errlen, RPG_E_PROFILE,
                    "T_max exceeds 1024, the architectural block limit");
-  if (hw->W_max > 16383 || hw->B_max > 4095)
+  if (hw->W_max > 16383 || hw->B_max > 4095 || hw->num_SM > 4095)
     return set_err(err, errlen, RPG_E_PROFILE,
-                   "profile: W_max above 16383 or B_max above 4095 is not supported");
+                   "profile: W_max above 16383, B_max or num_SM above 4095 is not supported");
   return RPG_OK;
 }
 
