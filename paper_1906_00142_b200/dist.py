@@ -1,0 +1,60 @@
+"""Multi-GPU sharding of a batched search along the data-parameter axis.
+
+Every (data tuple, config) point is independent and the argmin is per tuple
+(SURVEY.md 8e), so a sweep shards by contiguous blocks of data tuples — the
+same static partition the reference uses for its worker threads
+(``lo = n*j/jobs``, pipeline.hpp:602) — with no cross-rank tie merging.  The
+only exchange is one all-gather of the fixed-size 48-byte winner records.
+
+One process per GPU (``torch.distributed``; NCCL on GPUs, gloo for CPU
+tests).  ``search_fn`` evaluates one shard and returns its winner records
+(``abi.WINNER_DTYPE``); on a GPU it is ``Plan.search_batch`` (host buffers)
+or a device-buffer variant.
+"""
+from __future__ import annotations
+
+from typing import Callable, Tuple
+
+import numpy as np
+
+from . import abi as A
+
+
+def shard_range(n: int, world: int, rank: int) -> Tuple[int, int]:
+    """[lo, hi) of rank's contiguous block (pipeline.hpp:602 partition)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def sharded_search(data: np.ndarray, search_fn: Callable[[np.ndarray], np.ndarray],
+                   group=None) -> np.ndarray:
+    """Runs ``search_fn`` on this rank's block of ``data`` rows and
+    all-gathers the winners of every rank, in tuple order.  Returns the full
+    winner array on every rank (byte-identical to a single-process search)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = len(data)
+    lo, hi = shard_range(n, world, rank)
+    local = search_fn(np.ascontiguousarray(data[lo:hi]))
+    if local.dtype != A.WINNER_DTYPE or len(local) != hi - lo:
+        raise ValueError("search_fn must return one winner record per tuple")
+    # Fixed-size records; pad every block to the largest shard.
+    max_rows = max(shard_range(n, world, r)[1] - shard_range(n, world, r)[0] for r in range(world))
+    rec = A.WINNER_DTYPE.itemsize
+    backend = dist.get_backend(group)
+    device = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    buf = torch.zeros(max_rows * rec, dtype=torch.uint8, device=device)
+    if hi > lo:
+        buf[: (hi - lo) * rec] = torch.from_numpy(local.view(np.uint8).copy()).to(device)
+    out = torch.empty(world * max_rows * rec, dtype=torch.uint8, device=device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    allrec = out.cpu().numpy().reshape(world, max_rows * rec)
+    parts = []
+    for r in range(world):
+        a, b = shard_range(n, world, r)
+        parts.append(allrec[r, : (b - a) * rec])
+    return np.concatenate(parts).view(A.WINNER_DTYPE)
