@@ -220,6 +220,24 @@ int64_t rpg_emit_cuda_source(const rpg_model* model, const rpg_profile* hw,
                              size_t buflen, int64_t* cubin_bytes, char* err,
                              size_t errlen);
 
+/* poly::fit_rational (polyfit.hpp:337-427) on the GPU: the homogeneous
+ * least-squares rational fit of y over the points X (m x n_vars, row-major,
+ * host memory) with graded-lex numerator/denominator bases of the given
+ * per-variable degree bounds, including the reference's positivity safeguard.
+ * Outputs (host, caller-allocated): coef_out[n] (numerator coefficients then
+ * denominator coefficients, unit 2-norm, first |den| > 1e-10 positive),
+ * sigma_out[min(m, n)] (singular values of the equilibrated sample matrix,
+ * non-increasing), rank / truncated / residual as FitReport, safeguard_out =
+ * whether the safeguard ran.  Any output pointer may be NULL.
+ * Errors: RPG_E_INVALID (no samples, bad bounds, n > 64), RPG_E_FIT
+ * (DegenerateFit / SvdFailure messages of the reference). */
+int rpg_fit_rational(const double* X, const double* y, int64_t m, int32_t n_vars,
+                     const int32_t* num_bounds, const int32_t* den_bounds,
+                     double rank_tol, int32_t device, double* coef_out,
+                     double* sigma_out, int32_t* rank_out, int32_t* truncated_out,
+                     double* residual_out, int32_t* safeguard_out, char* err,
+                     size_t errlen);
+
 /* One-shot convenience for FFI callers. */
 int rpg_search(const rpg_model* model, const rpg_profile* hw,
                const rpg_config* space, int64_t n_space,

@@ -85,8 +85,10 @@ class SvdResult:
 def svd(A: np.ndarray) -> SvdResult:
     if not np.all(np.isfinite(A)):
         raise SvdFailure("svd: matrix has non-finite entries")
+    m, n = A.shape
     try:
-        U, s, Vh = np.linalg.svd(A, full_matrices=True)
+        # thin U; V must be full n x n (only m < n needs full_matrices)
+        U, s, Vh = np.linalg.svd(A, full_matrices=m < n)
     except np.linalg.LinAlgError:
         raise SvdFailure("svd: decomposition did not converge") from None
     k = len(s)

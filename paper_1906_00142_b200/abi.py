@@ -198,6 +198,12 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "rpg_emit_cuda_source": (C.c_int64, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
                                              C.POINTER(rpg_options), C.c_int32, C.c_char_p,
                                              C.c_size_t, C.POINTER(C.c_int64)) + errbuf),
+        "rpg_fit_rational": (C.c_int, (C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64,
+                                       C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                       C.c_double, C.c_int32, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_int32)) + errbuf),
         "rpg_search": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
                                  C.POINTER(rpg_config), C.c_int64,
                                  C.POINTER(rpg_options), C.POINTER(C.c_int64),
@@ -214,7 +220,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_plan_destroy", "rpg_search_batch",
                     "rpg_search_batch_device", "rpg_evaluate",
-                    "rpg_evaluate_device", "rpg_search", "rpg_emit_cuda_source")
+                    "rpg_evaluate_device", "rpg_search", "rpg_emit_cuda_source",
+                    "rpg_fit_rational")
 
 
 class RpgError(RuntimeError):

@@ -344,3 +344,863 @@ __global__ void den_stats(const FitParams F, const double* __restrict__ cden,
 }
 
 }  // namespace rpg_fit
+
+namespace rpg_fit {
+
+// Final small reductions / normalisation on the device (one warp-sized CTA).
+// stats: G x 4 partials of den_stats.  out_flags[0]: safeguard trigger.
+__global__ void den_stats_final(const double* __restrict__ partial, int G, int64_t m,
+                                int* __restrict__ trigger, double* __restrict__ stats) {
+  if (threadIdx.x != 0) return;
+  double qmin = INFINITY, nqmax = INFINITY, asum = 0.0, amin = INFINITY;
+  for (int g = 0; g < G; ++g) {
+    qmin = fmin(qmin, partial[g * 4 + 0]);
+    nqmax = fmin(nqmax, partial[g * 4 + 1]);
+    asum += partial[g * 4 + 2];
+    amin = fmin(amin, partial[g * 4 + 3]);
+  }
+  const double qmax = -nqmax;
+  const double mean_mag = asum / (double)m;
+  // polyfit.hpp:375-378
+  const bool sign_mixed = qmin < 0.0 && qmax > 0.0;
+  const bool pinched = mean_mag > 0.0 && amin < 1e-4 * mean_mag;
+  *trigger = (sign_mixed || pinched) ? 1 : 0;
+  stats[0] = qmin;
+  stats[1] = qmax;
+  stats[2] = mean_mag;
+  stats[3] = amin;
+}
+
+// make_ratfunc_from_coeffs (polyfit.hpp:185-213) + numerical_rank
+// (polyfit.hpp:171-177).  status: 0 ok, 1 all-zero vector, 2 zero denominator.
+__global__ void fit_finalize(double* __restrict__ c, int nn, int nd, const double* __restrict__ sigma,
+                             int nsig, double rank_tol, int* __restrict__ status,
+                             int* __restrict__ rank) {
+  if (threadIdx.x != 0) return;
+  const int n = nn + nd;
+  double s = 0.0;
+  for (int k = 0; k < n; ++k) s = fma(c[k], c[k], s);
+  const double norm = sqrt(s);
+  int r = 0;
+  if (nsig > 0 && sigma[0] > 0.0)
+    for (int i = 0; i < nsig; ++i) r += sigma[i] >= rank_tol * sigma[0];
+  *rank = r;
+  if (norm == 0.0) {
+    *status = 1;
+    return;
+  }
+  for (int k = 0; k < n; ++k) c[k] /= norm;
+  int first = -1;
+  for (int j = 0; j < nd; ++j)
+    if (fabs(c[nn + j]) > 1e-10) {
+      first = j;
+      break;
+    }
+  if (first < 0) {
+    *status = 2;
+    return;
+  }
+  if (c[nn + first] < 0.0)
+    for (int k = 0; k < n; ++k) c[k] = -c[k];
+  *status = 0;
+}
+
+__global__ void smallest_vector(const double* __restrict__ V, const double* __restrict__ col_scale,
+                                int n, double* __restrict__ c) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) c[i] = V[(n - 1) * n + i] * col_scale[i];
+}
+
+__global__ void all_finite(const double* __restrict__ a, int64_t count, int* __restrict__ bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(a[i])) *bad = 1;
+}
+
+}  // namespace rpg_fit
+
+namespace rpg_fit {
+
+// ---------------------------------------------------------------------------
+// Positivity safeguard (polyfit.hpp:242-311, 369-414) — device kernels.
+
+// Column sums of the denominator monomials: g = Q.colwise().sum() / S_den.
+__global__ void den_colsum(const FitParams F, double* __restrict__ partial) {
+  extern __shared__ __align__(16) double fsm[];
+  double* acc = fsm;  // nd x (blockDim/32)
+  uint8_t* sexps = reinterpret_cast<uint8_t*>(acc + kMaxCols * kFitWarps);
+  for (int e = threadIdx.x; e < F.nd * F.n_vars; e += blockDim.x)
+    sexps[e] = F.exps[F.nn * F.n_vars + e];
+  __syncthreads();
+  double loc[kMaxCols];
+  for (int k = 0; k < F.nd; ++k) loc[k] = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < F.m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double x[RPG_MAX_VARS];
+    for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
+    for (int k = 0; k < F.nd; ++k) loc[k] += monomial(x, sexps + k * F.n_vars, F.n_vars);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int k = 0; k < F.nd; ++k) {
+    double t = loc[k];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (l == 0) acc[k * kFitWarps + w] = t;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < F.nd; k += blockDim.x) {
+    double t = 0.0;
+    for (int i = 0; i < kFitWarps; ++i) t += acc[k * kFitWarps + i];
+    partial[(size_t)blockIdx.x * F.nd + k] = t;
+  }
+}
+
+// One pass over the samples for the denominator values q_k = D_k . cd
+// (cd: raw-coordinate denominator coefficients) at up to kAlphas candidate
+// vectors cd + alpha_a * dd: per candidate min q and sum log q; with
+// `newton`, for candidate 0 also sum (1/q) D_k and sum (1/q^2) D_k D_k^T.
+constexpr int kAlphas = 4;
+constexpr int kPassRows = 256;
+
+__global__ void __launch_bounds__(kFitThreads)
+den_pass(const FitParams F, const double* __restrict__ cd, const double* __restrict__ dd,
+         const double* __restrict__ alphas, int n_alpha, int newton,
+         double* __restrict__ partial /* per block: 2*kAlphas + nd + nd*nd */) {
+  extern __shared__ __align__(16) double fsm[];
+  const int nd = F.nd;
+  double* U = fsm;                                  // kPassRows x nd (row-major)
+  double* red = U + kPassRows * kMaxCols;           // 32
+  double* cands = red + 32;                         // kAlphas x nd
+  uint8_t* sexps = reinterpret_cast<uint8_t*>(cands + kAlphas * kMaxCols);
+  for (int e = threadIdx.x; e < nd * F.n_vars; e += blockDim.x)
+    sexps[e] = F.exps[F.nn * F.n_vars + e];
+  for (int e = threadIdx.x; e < n_alpha * nd; e += blockDim.x) {
+    const int a = e / nd, k = e % nd;
+    cands[e] = dd ? cd[k] + alphas[a] * dd[k] : cd[k];
+  }
+  __syncthreads();
+  double qmin[kAlphas], slog[kAlphas];
+  for (int a = 0; a < kAlphas; ++a) {
+    qmin[a] = INFINITY;
+    slog[a] = 0.0;
+  }
+  // Gram accumulators: thread t owns entries t, t+blockDim, ... of nd x nd
+  double gacc[16];
+  for (int i = 0; i < 16; ++i) gacc[i] = 0.0;
+  double gq = 0.0;  // thread t < nd owns sum (1/q) D[t]
+  const int64_t nrow_tiles = (F.m + kPassRows - 1) / kPassRows;
+  for (int64_t tile = blockIdx.x; tile < nrow_tiles; tile += gridDim.x) {
+    const int64_t r = tile * kPassRows + threadIdx.x;
+    const bool valid = threadIdx.x < kPassRows && r < F.m;
+    double D[kMaxCols];
+    if (valid) {
+      double x[RPG_MAX_VARS];
+      for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
+      for (int k = 0; k < nd; ++k) D[k] = monomial(x, sexps + k * F.n_vars, F.n_vars);
+      for (int a = 0; a < n_alpha; ++a) {
+        double q = 0.0;
+        for (int k = 0; k < nd; ++k) q = fma(D[k], cands[a * nd + k], q);
+        qmin[a] = fmin(qmin[a], q);
+        slog[a] += log(q);
+      }
+    }
+    if (newton) {
+      __syncthreads();
+      if (threadIdx.x < kPassRows) {
+        double q = 0.0, qi = 0.0;
+        if (valid) {
+          for (int k = 0; k < nd; ++k) q = fma(D[k], cands[k], q);
+          qi = 1.0 / q;
+        }
+        for (int k = 0; k < nd; ++k) U[threadIdx.x * nd + k] = valid ? D[k] * qi : 0.0;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x, i = 0; e < nd * nd; e += blockDim.x, ++i) {
+        const int a = e / nd, b = e % nd;
+        double t = 0.0;
+        for (int row = 0; row < kPassRows; ++row) t = fma(U[row * nd + a], U[row * nd + b], t);
+        gacc[i] += t;
+      }
+      if ((int)threadIdx.x < nd) {
+        // sum_k (1/q_k) D_k[t] = sum of column t of U
+        double t = 0.0;
+        for (int row = 0; row < kPassRows; ++row) t += U[row * nd + threadIdx.x];
+        gq += t;
+      }
+    }
+  }
+  double* out = partial + (size_t)blockIdx.x * (2 * kAlphas + nd + nd * nd);
+  for (int a = 0; a < kAlphas; ++a) {
+    double t = qmin[a], u = slog[a];
+    for (int o = 16; o > 0; o >>= 1) {
+      t = fmin(t, __shfl_xor_sync(0xffffffffu, t, o));
+      u += __shfl_xor_sync(0xffffffffu, u, o);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      red[threadIdx.x >> 5] = t;
+      red[16 + (threadIdx.x >> 5)] = u;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mn = red[0], sm = red[16];
+      for (int i = 1; i < kFitWarps; ++i) {
+        mn = fmin(mn, red[i]);
+        sm += red[16 + i];
+      }
+      out[2 * a] = mn;
+      out[2 * a + 1] = sm;
+    }
+  }
+  if (newton) {
+    if ((int)threadIdx.x < nd) out[2 * kAlphas + threadIdx.x] = gq;
+    for (int e = threadIdx.x, i = 0; e < nd * nd; e += blockDim.x, ++i)
+      out[2 * kAlphas + nd + e] = gacc[i];
+  }
+}
+
+// Sums the per-block partials of den_pass (min for the q minima).
+__global__ void den_pass_final(const double* __restrict__ partial, int G, int nd,
+                               double* __restrict__ out) {
+  const int W = 2 * kAlphas + nd + nd * nd;
+  for (int e = threadIdx.x; e < W; e += blockDim.x) {
+    const bool is_min = e < 2 * kAlphas && (e % 2) == 0;
+    double t = is_min ? INFINITY : 0.0;
+    for (int g = 0; g < G; ++g) t = is_min ? fmin(t, partial[(size_t)g * W + e]) : t + partial[(size_t)g * W + e];
+    out[e] = t;
+  }
+}
+
+// ||R S v||^2 for the n x n upper-triangular R (row-major) and scale S.
+__device__ double rs_norm2(const double* R, const double* S, const double* v, int n) {
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double t = 0.0;
+    for (int k = i; k < n; ++k) t = fma(R[i * n + k], S[k] * v[k], t);
+    acc = fma(t, t, acc);
+  }
+  return acc;
+}
+
+// Minimizer state (device): c (n, equilibrated coordinates), dc (n), scalars.
+struct MinState {
+  double mu, phi0, decrement;
+  int ok;
+};
+
+// Setup: c = start / S, q = Q c must be > 0, rescale so g.c = m, mu.
+// pass_out: den_pass of the raw start's denominator (min q at index 0).
+__global__ void min_setup(const double* __restrict__ R, const double* __restrict__ S,
+                          const double* __restrict__ start, const double* __restrict__ gsum,
+                          const double* __restrict__ pass_out, int nn, int nd, int64_t m,
+                          double* __restrict__ c, MinState* __restrict__ st) {
+  if (threadIdx.x != 0) return;
+  const int n = nn + nd;
+  for (int k = 0; k < n; ++k) c[k] = start[k] / S[k];
+  st->ok = 0;
+  if (!(pass_out[0] > 0.0)) return;
+  // g = Q.colwise().sum(): den block = S_den .* colsum(D)
+  double gc = 0.0;
+  for (int k = 0; k < nd; ++k) gc = fma(gsum[k] * S[nn + k], c[nn + k], gc);
+  const double s = (double)m / gc;
+  if (!(s > 0.0) || !isfinite(s)) return;
+  for (int k = 0; k < n; ++k) c[k] *= s;
+  const double a2 = rs_norm2(R, S, c, n);
+  st->mu = fmax(a2, 1e-30) / (double)m;
+  st->ok = 1;
+}
+
+// Raw-coordinate denominator coefficients (S_den .* c_den) and direction.
+__global__ void raw_den(const double* __restrict__ c, const double* __restrict__ dc,
+                        const double* __restrict__ S, int nn, int nd, double* __restrict__ cd,
+                        double* __restrict__ dd) {
+  for (int k = threadIdx.x; k < nd; k += blockDim.x) {
+    cd[k] = S[nn + k] * c[nn + k];
+    if (dc && dd) dd[k] = S[nn + k] * dc[nn + k];
+  }
+}
+
+// Newton step: grad = 2 H0 c - mu Q^T(1/q), H = 2 H0 + mu Q^T diag(1/q^2) Q,
+// KKT [H g; g^T 0] [dc; l] = [-grad; 0] solved by Gaussian elimination with
+// partial pivoting (the reference uses LDLT), decrement = -grad.dc,
+// phi0 = ||A_eq c||^2 - mu sum log q.  One CTA.
+__global__ void __launch_bounds__(kFitThreads)
+newton_step(const double* __restrict__ R, const double* __restrict__ S,
+            const double* __restrict__ gsum, const double* __restrict__ pass_out,
+            const double* __restrict__ c, int nn, int nd, double* __restrict__ dc,
+            MinState* __restrict__ st) {
+  extern __shared__ __align__(16) double fsm[];
+  const int n = nn + nd, N = n + 1;
+  double* K = fsm;                 // N x (N+1) augmented, row-major
+  double* H0c = K + N * (N + 1);   // n
+  double* RSc = H0c + n;           // n: (R S c)
+  double* grad = RSc + n;          // n
+  const double mu = st->mu;
+  const double* gq = pass_out + 2 * kAlphas;
+  const double* G = gq + nd;
+  // RSc = R S c
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double t = 0.0;
+    for (int k = i; k < n; ++k) t = fma(R[i * n + k], S[k] * c[k], t);
+    RSc[i] = t;
+  }
+  __syncthreads();
+  // H0 c = S R^T (R S c)
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    double t = 0.0;
+    for (int i = 0; i <= k; ++i) t = fma(R[i * n + k], RSc[i], t);
+    H0c[k] = S[k] * t;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    double qterm = k >= nn ? S[k] * gq[k - nn] : 0.0;
+    grad[k] = 2.0 * H0c[k] - mu * qterm;
+  }
+  // H entries
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int a = e / n, b = e % n;
+    double h = 0.0;
+    for (int i = 0; i <= (a < b ? a : b); ++i) h = fma(R[i * n + a], R[i * n + b], h);
+    h = 2.0 * S[a] * S[b] * h;
+    if (a >= nn && b >= nn) h += mu * S[a] * S[b] * G[(a - nn) * nd + (b - nn)];
+    K[a * (N + 1) + b] = h;
+  }
+  for (int a = threadIdx.x; a < n; a += blockDim.x) {
+    const double g = a >= nn ? gsum[a - nn] * S[a] : 0.0;
+    K[a * (N + 1) + n] = g;
+    K[n * (N + 1) + a] = g;
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < n; a += blockDim.x) K[a * (N + 1) + N] = -grad[a];
+  if (threadIdx.x == 0) {
+    K[n * (N + 1) + n] = 0.0;
+    K[n * (N + 1) + N] = 0.0;
+  }
+  __syncthreads();
+  // Gaussian elimination with partial pivoting (single thread picks the
+  // pivot, all threads eliminate).
+  __shared__ int piv;
+  __shared__ int singular;
+  if (threadIdx.x == 0) singular = 0;
+  for (int col = 0; col < N; ++col) {
+    if (threadIdx.x == 0) {
+      int p = col;
+      double best = fabs(K[col * (N + 1) + col]);
+      for (int r = col + 1; r < N; ++r)
+        if (fabs(K[r * (N + 1) + col]) > best) {
+          best = fabs(K[r * (N + 1) + col]);
+          p = r;
+        }
+      piv = p;
+      if (best == 0.0) singular = 1;
+    }
+    __syncthreads();
+    if (piv != col)
+      for (int j = threadIdx.x; j <= N; j += blockDim.x) {
+        const double t = K[col * (N + 1) + j];
+        K[col * (N + 1) + j] = K[piv * (N + 1) + j];
+        K[piv * (N + 1) + j] = t;
+      }
+    __syncthreads();
+    const double d = K[col * (N + 1) + col];
+    for (int e = threadIdx.x; e < (N - col - 1) * (N - col); e += blockDim.x) {
+      const int r = col + 1 + e / (N - col), j = col + 1 + e % (N - col);
+      const double f = K[r * (N + 1) + col] / d;
+      K[r * (N + 1) + j] -= f * K[col * (N + 1) + j];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double x[kMaxCols + 1];
+    for (int r = N - 1; r >= 0; --r) {
+      double t = K[r * (N + 1) + N];
+      for (int j = r + 1; j < N; ++j) t -= K[r * (N + 1) + j] * x[j];
+      x[r] = t / K[r * (N + 1) + r];
+    }
+    bool finite = !singular;
+    double dec = 0.0;
+    for (int k = 0; k < n; ++k) {
+      dc[k] = x[k];
+      finite &= isfinite(x[k]);
+      dec = fma(-grad[k], x[k], dec);
+    }
+    st->ok = finite ? 1 : 0;
+    st->decrement = dec;
+    double a2 = 0.0;
+    for (int i = 0; i < n; ++i) a2 = fma(RSc[i], RSc[i], a2);
+    st->phi0 = a2 - mu * pass_out[1];
+  }
+}
+
+// phi(c + alpha dc) for the candidate alphas: ||R S cn||^2 - mu sum log qn.
+__global__ void line_phi(const double* __restrict__ R, const double* __restrict__ S,
+                         const double* __restrict__ c, const double* __restrict__ dc,
+                         const double* __restrict__ alphas, int n_alpha, int n,
+                         const double* __restrict__ pass_out, const MinState* __restrict__ st,
+                         double* __restrict__ phis) {
+  const int a = threadIdx.x;
+  if (a >= n_alpha) return;
+  double cn[kMaxCols];
+  for (int k = 0; k < n; ++k) cn[k] = c[k] + alphas[a] * dc[k];
+  phis[a] = rs_norm2(R, S, cn, n) - st->mu * pass_out[2 * a + 1];
+}
+
+__global__ void axpy_small(double* __restrict__ c, const double* __restrict__ dc, double alpha, int n) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) c[k] += alpha * dc[k];
+}
+
+__global__ void to_raw(const double* __restrict__ c, const double* __restrict__ S, int n,
+                       double* __restrict__ raw, int* __restrict__ finite) {
+  if (threadIdx.x != 0) return;
+  int f = 1;
+  for (int k = 0; k < n; ++k) {
+    raw[k] = c[k] * S[k];
+    f &= isfinite(raw[k]) ? 1 : 0;
+  }
+  *finite = f;
+}
+
+// Row weights of the reweighted rounds: max(1, |y_k|) * qprev_k.
+__global__ void row_weights(const FitParams F, const double* __restrict__ cd,
+                            double* __restrict__ w) {
+  extern __shared__ __align__(16) double fsm[];
+  uint8_t* sexps = reinterpret_cast<uint8_t*>(fsm);
+  for (int e = threadIdx.x; e < F.nd * F.n_vars; e += blockDim.x)
+    sexps[e] = F.exps[F.nn * F.n_vars + e];
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < F.m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double x[RPG_MAX_VARS];
+    for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
+    double q = 0.0;
+    for (int k = 0; k < F.nd; ++k) q = fma(monomial(x, sexps + k * F.n_vars, F.n_vars), cd[k], q);
+    w[r] = fmax(1.0, fabs(F.y[r])) * q;
+  }
+}
+
+// Start vector of the safeguard from the SVD of R_v (the R factor of the
+// numerator-only matrix V) and z = (Q_v^T y)[0:nn]: start[0:nn] =
+// sum_{i<rank} W_i (u_i . z) / sigma_i, start[nn] = 1 (polyfit.hpp:382-395).
+__global__ void start_vector(const double* __restrict__ Wv, const double* __restrict__ Uv,
+                             const double* __restrict__ sig, const double* __restrict__ z,
+                             int nn, int nd, double rank_tol, double* __restrict__ start) {
+  if (threadIdx.x != 0) return;
+  int rank = 0;
+  if (nn > 0 && sig[0] > 0.0)
+    for (int i = 0; i < nn; ++i) rank += sig[i] >= rank_tol * sig[0];
+  for (int k = 0; k < nn + nd; ++k) start[k] = 0.0;
+  for (int i = 0; i < rank; ++i) {
+    double uty = 0.0;
+    for (int j = 0; j < nn; ++j) uty = fma(Uv[i * nn + j], z[j], uty);
+    const double f = uty / sig[i];
+    for (int k = 0; k < nn; ++k) start[k] = fma(Wv[i * nn + k], f, start[k]);
+  }
+  start[nn] = 1.0;
+}
+
+// 1 / column norms of an R factor (equilibrate_columns, polyfit.hpp:219-229).
+__global__ void col_scale_from_R(const double* __restrict__ R, int n, double* __restrict__ S) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    double t = 0.0;
+    for (int i = 0; i <= k; ++i) t = fma(R[i * n + k], R[i * n + k], t);
+    const double cn = sqrt(t);
+    S[k] = cn > 0.0 ? 1.0 / cn : 1.0;
+  }
+}
+
+__global__ void sum_partials(const double* __restrict__ partial, int G, int width,
+                             double* __restrict__ out) {
+  for (int k = threadIdx.x; k < width; k += blockDim.x) {
+    double t = 0.0;
+    for (int g = 0; g < G; ++g) t += partial[(size_t)g * width + k];
+    out[k] = t;
+  }
+}
+
+// Splits the (nn+1) x (nn+1) R factor of [V | y] into R_v and z.
+__global__ void split_vy(const double* __restrict__ Rvy, int nn, double* __restrict__ Rv,
+                         double* __restrict__ z) {
+  const int N = nn + 1;
+  for (int e = threadIdx.x; e < nn * nn; e += blockDim.x) Rv[e] = Rvy[(e / nn) * N + (e % nn)];
+  for (int j = threadIdx.x; j < nn; j += blockDim.x) z[j] = Rvy[j * N + nn];
+}
+
+}  // namespace rpg_fit
+
+// ---------------------------------------------------------------------------
+// Host orchestration + C ABI.
+
+namespace {
+
+using namespace rpg_fit;
+
+int fset_err(char* err, size_t errlen, int code, const char* fmt, ...) {
+  if (err && errlen) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(err, errlen, fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+std::vector<std::vector<int>> basis(const int32_t* bounds, int nv) {
+  std::vector<std::vector<int>> tuples{{}};
+  for (int v = 0; v < nv; ++v) {
+    std::vector<std::vector<int>> next;
+    for (const auto& t : tuples)
+      for (int e = 0; e <= bounds[v]; ++e) {
+        next.push_back(t);
+        next.back().push_back(e);
+      }
+    tuples.swap(next);
+  }
+  std::stable_sort(tuples.begin(), tuples.end(), [](const std::vector<int>& a, const std::vector<int>& b) {
+    int ga = 0, gb = 0;
+    for (int x : a) ga += x;
+    for (int x : b) gb += x;
+    if (ga != gb) return ga < gb;
+    return a < b;
+  });
+  return tuples;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+#define FCUDA(expr)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fset_err(err, errlen, RPG_E_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+size_t tsqr_smem(int n_vars) {
+  return sizeof(double) * ((size_t)kMaxCols * kMaxCols + (size_t)kTile * kMaxCols + 32 + kMaxCols) +
+         (size_t)kMaxCols * RPG_MAX_VARS + 16;
+}
+
+// R factor (n x n, row-major, in *Rdev) of the sample matrix described by F.
+int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, char* err,
+         size_t errlen) {
+  const int64_t tiles = (F.m + kTile - 1) / kTile;
+  int G = (int)std::min<int64_t>(tiles, 2LL * sms);
+  if (G < 1) G = 1;
+  FCUDA(cudaMalloc(&Rbuf->p, sizeof(double) * (size_t)G * ncols * ncols));
+  const size_t sm1 = tsqr_smem(F.n_vars);
+  FCUDA(cudaFuncSetAttribute(tsqr_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+  tsqr_tiles<<<G, kFitThreads, sm1, s>>>(F, Rbuf->as<double>());
+  FCUDA(cudaGetLastError());
+  const size_t sm2 = sizeof(double) * (2 * (size_t)kMaxCols * kMaxCols + 32 + kMaxCols);
+  FCUDA(cudaFuncSetAttribute(tsqr_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  // Tree over the G factors: at every level slot 2b absorbs slot 2b+1; then
+  // survivors are compacted by re-striding (slot 2b -> b) with a copy.
+  int count = G;
+  DevBuf tmp;
+  FCUDA(cudaMalloc(&tmp.p, sizeof(double) * (size_t)G * ncols * ncols));
+  while (count > 1) {
+    tsqr_combine<<<count / 2, kFitThreads, sm2, s>>>(Rbuf->as<double>(), count, ncols);
+    FCUDA(cudaGetLastError());
+    const int next = (count + 1) / 2;
+    for (int b = 0; b < next; ++b)
+      FCUDA(cudaMemcpyAsync(tmp.as<double>() + (size_t)b * ncols * ncols,
+                            Rbuf->as<double>() + (size_t)(2 * b) * ncols * ncols,
+                            sizeof(double) * ncols * ncols, cudaMemcpyDeviceToDevice, s));
+    FCUDA(cudaMemcpyAsync(Rbuf->p, tmp.p, sizeof(double) * (size_t)next * ncols * ncols,
+                          cudaMemcpyDeviceToDevice, s));
+    count = next;
+  }
+  return RPG_OK;
+}
+
+}  // namespace
+
+struct Pass {
+  DevBuf part, out;
+  int G = 0, nd = 0;
+};
+
+int run_den_pass(const FitParams& F, const double* cd, const double* dd, const double* alphas,
+                 int n_alpha, int newton, int sms, Pass* P, cudaStream_t s, char* err,
+                 size_t errlen) {
+  const int W = 2 * kAlphas + F.nd + F.nd * F.nd;
+  if (!P->part.p) {
+    const int64_t tiles = (F.m + kPassRows - 1) / kPassRows;
+    P->G = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2LL * sms));
+    P->nd = F.nd;
+    FCUDA(cudaMalloc(&P->part.p, sizeof(double) * (size_t)P->G * W));
+    FCUDA(cudaMalloc(&P->out.p, sizeof(double) * W));
+  }
+  const size_t sm = sizeof(double) * ((size_t)kPassRows * kMaxCols + 32 + kAlphas * kMaxCols) +
+                    (size_t)kMaxCols * RPG_MAX_VARS + 16;
+  FCUDA(cudaFuncSetAttribute(den_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  den_pass<<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>());
+  FCUDA(cudaGetLastError());
+  den_pass_final<<<1, 256, 0, s>>>(P->part.as<double>(), P->G, F.nd, P->out.as<double>());
+  return RPG_OK;
+}
+
+// positive_den_minimizer (polyfit.hpp:242-311).  R, S: R factor and column
+// scale of the (weighted) sample matrix; gsum: column sums of the raw
+// denominator monomials; start (raw coordinates).  *found = 0 when the
+// reference would return an empty vector.
+int minimizer(const FitParams& F, const double* R, const double* S, const double* gsum,
+              const double* start, double* out_raw, int* found, int sms, cudaStream_t s,
+              char* err, size_t errlen) {
+  const int nn = F.nn, nd = F.nd, n = F.n;
+  *found = 0;
+  DevBuf c, dc, cd, dd, alphas, st, phis, fin;
+  FCUDA(cudaMalloc(&c.p, sizeof(double) * n));
+  FCUDA(cudaMalloc(&dc.p, sizeof(double) * n));
+  FCUDA(cudaMalloc(&cd.p, sizeof(double) * nd));
+  FCUDA(cudaMalloc(&dd.p, sizeof(double) * nd));
+  FCUDA(cudaMalloc(&alphas.p, sizeof(double) * kAlphas));
+  FCUDA(cudaMalloc(&st.p, sizeof(MinState)));
+  FCUDA(cudaMalloc(&phis.p, sizeof(double) * kAlphas));
+  FCUDA(cudaMalloc(&fin.p, sizeof(int)));
+  Pass P;
+  // q of the start vector: Q (start / S) = D start_den.
+  FCUDA(cudaMemcpyAsync(cd.p, start + nn, sizeof(double) * nd, cudaMemcpyDeviceToDevice, s));
+  int rc = run_den_pass(F, cd.as<double>(), nullptr, nullptr, 1, 0, sms, &P, s, err, errlen);
+  if (rc) return rc;
+  min_setup<<<1, 32, 0, s>>>(R, S, start, gsum, P.out.as<double>(), nn, nd, F.m, c.as<double>(),
+                             st.as<MinState>());
+  MinState hs;
+  FCUDA(cudaMemcpyAsync(&hs, st.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  FCUDA(cudaStreamSynchronize(s));
+  if (!hs.ok) return RPG_OK;
+  double mu = hs.mu;
+  const size_t smk = sizeof(double) * ((size_t)(kMaxCols + 1) * (kMaxCols + 2) + 3 * kMaxCols);
+  FCUDA(cudaFuncSetAttribute(newton_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smk));
+  for (int outer = 0; outer < 16; ++outer) {
+    for (int inner = 0; inner < 40; ++inner) {
+      raw_den<<<1, 64, 0, s>>>(c.as<double>(), nullptr, S, nn, nd, cd.as<double>(), nullptr);
+      rc = run_den_pass(F, cd.as<double>(), nullptr, nullptr, 1, 1, sms, &P, s, err, errlen);
+      if (rc) return rc;
+      newton_step<<<1, kFitThreads, smk, s>>>(R, S, gsum, P.out.as<double>(), c.as<double>(), nn,
+                                               nd, dc.as<double>(), st.as<MinState>());
+      FCUDA(cudaGetLastError());
+      FCUDA(cudaMemcpyAsync(&hs, st.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+      FCUDA(cudaStreamSynchronize(s));
+      if (!hs.ok) return RPG_OK;  // non-finite KKT solution: empty result
+      if (!(hs.decrement > 1e-14 * (1.0 + std::fabs(hs.phi0)))) break;
+      bool stepped = false;
+      double alpha = 1.0;
+      raw_den<<<1, 64, 0, s>>>(c.as<double>(), dc.as<double>(), S, nn, nd, cd.as<double>(),
+                               dd.as<double>());
+      while (alpha > 1e-18 && !stepped) {
+        double al[kAlphas];
+        int na = 0;
+        for (double a = alpha; na < kAlphas && a > 1e-18; a *= 0.5) al[na++] = a;
+        FCUDA(cudaMemcpyAsync(alphas.p, al, sizeof(double) * na, cudaMemcpyHostToDevice, s));
+        rc = run_den_pass(F, cd.as<double>(), dd.as<double>(), alphas.as<double>(), na, 0, sms, &P,
+                          s, err, errlen);
+        if (rc) return rc;
+        line_phi<<<1, 32, 0, s>>>(R, S, c.as<double>(), dc.as<double>(), alphas.as<double>(), na, n,
+                                  P.out.as<double>(), st.as<MinState>(), phis.as<double>());
+        double po[2 * kAlphas], ph[kAlphas];
+        FCUDA(cudaMemcpyAsync(po, P.out.p, sizeof(po), cudaMemcpyDeviceToHost, s));
+        FCUDA(cudaMemcpyAsync(ph, phis.p, sizeof(double) * na, cudaMemcpyDeviceToHost, s));
+        FCUDA(cudaStreamSynchronize(s));
+        for (int a = 0; a < na; ++a) {
+          if (po[2 * a] > 0.0 && ph[a] <= hs.phi0 - 1e-4 * al[a] * hs.decrement) {
+            axpy_small<<<1, 64, 0, s>>>(c.as<double>(), dc.as<double>(), al[a], n);
+            stepped = true;
+            break;
+          }
+        }
+        alpha = al[na - 1] * 0.5;
+      }
+      if (!stepped) break;
+    }
+    mu *= 0.1;
+    MinState upd = hs;
+    upd.mu = mu;
+    FCUDA(cudaMemcpyAsync(st.p, &upd, sizeof(upd), cudaMemcpyHostToDevice, s));
+  }
+  to_raw<<<1, 32, 0, s>>>(c.as<double>(), S, n, out_raw, fin.as<int>());
+  int f = 0;
+  FCUDA(cudaMemcpyAsync(&f, fin.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FCUDA(cudaStreamSynchronize(s));
+  *found = f;
+  return RPG_OK;
+}
+
+// The positivity safeguard (polyfit.hpp:369-414).  c: in = the unconstrained
+// candidate (raw coordinates), out = the refined vector when one is found.
+int rpg_fit_safeguard(const FitParams& F, const double* R, const double* S, double* c,
+                      double rank_tol, int sms, cudaStream_t s, char* err, size_t errlen) {
+  const int nn = F.nn, nd = F.nd, n = F.n;
+  DevBuf gpart, gsum, Rvy, Rv, z, sv, Wv, Uv, dummy, start, refined, next, w, Rw, Sw;
+  // column sums of the raw denominator monomials
+  const int G = std::max(1, std::min<int>((int)((F.m + 255) / 256), 2 * sms));
+  FCUDA(cudaMalloc(&gpart.p, sizeof(double) * (size_t)G * nd));
+  FCUDA(cudaMalloc(&gsum.p, sizeof(double) * nd));
+  const size_t smc = sizeof(double) * kMaxCols * kFitWarps + (size_t)kMaxCols * RPG_MAX_VARS + 16;
+  FCUDA(cudaFuncSetAttribute(den_colsum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc));
+  den_colsum<<<G, kFitThreads, smc, s>>>(F, gpart.as<double>());
+  sum_partials<<<1, 64, 0, s>>>(gpart.as<double>(), G, nd, gsum.as<double>());
+  // start vector: least squares of the numerator basis against y
+  FitParams Fv = F;
+  Fv.num_only = 1;
+  Fv.with_y_col = 1;
+  int rc = tsqr(Fv, nn + 1, sms, &Rvy, s, err, errlen);
+  if (rc) return rc;
+  FCUDA(cudaMalloc(&Rv.p, sizeof(double) * nn * nn));
+  FCUDA(cudaMalloc(&z.p, sizeof(double) * nn));
+  split_vy<<<1, 128, 0, s>>>(Rvy.as<double>(), nn, Rv.as<double>(), z.as<double>());
+  FCUDA(cudaMalloc(&sv.p, sizeof(double) * nn));
+  FCUDA(cudaMalloc(&Wv.p, sizeof(double) * nn * nn));
+  FCUDA(cudaMalloc(&Uv.p, sizeof(double) * nn * nn));
+  FCUDA(cudaMalloc(&dummy.p, sizeof(double) * nn));
+  const size_t sm3 = sizeof(double) * (2 * (size_t)kMaxCols * kMaxCols + kMaxCols) + sizeof(int) * (kMaxCols + 4);
+  svd_small<<<1, kFitThreads, sm3, s>>>(Rv.as<double>(), nn, sv.as<double>(), Wv.as<double>(),
+                                        dummy.as<double>(), Uv.as<double>(), 0);
+  FCUDA(cudaMalloc(&start.p, sizeof(double) * n));
+  start_vector<<<1, 32, 0, s>>>(Wv.as<double>(), Uv.as<double>(), sv.as<double>(), z.as<double>(),
+                                nn, nd, rank_tol, start.as<double>());
+  FCUDA(cudaMalloc(&refined.p, sizeof(double) * n));
+  FCUDA(cudaMalloc(&next.p, sizeof(double) * n));
+  int found = 0;
+  rc = minimizer(F, R, S, gsum.as<double>(), start.as<double>(), refined.as<double>(), &found, sms,
+                 s, err, errlen);
+  if (rc) return rc;
+  FCUDA(cudaMalloc(&w.p, sizeof(double) * (size_t)F.m));
+  FCUDA(cudaMalloc(&Sw.p, sizeof(double) * n));
+  DevBuf cdp;
+  FCUDA(cudaMalloc(&cdp.p, sizeof(double) * nd));
+  Pass P;
+  for (int round = 0; found && round < 3; ++round) {
+    FCUDA(cudaMemcpyAsync(cdp.p, refined.as<double>() + nn, sizeof(double) * nd,
+                          cudaMemcpyDeviceToDevice, s));
+    rc = run_den_pass(F, cdp.as<double>(), nullptr, nullptr, 1, 0, sms, &P, s, err, errlen);
+    if (rc) return rc;
+    double qmin = 0.0;
+    FCUDA(cudaMemcpyAsync(&qmin, P.out.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    FCUDA(cudaStreamSynchronize(s));
+    if (!(qmin > 0.0)) break;
+    const size_t smw = (size_t)kMaxCols * RPG_MAX_VARS + 16;
+    row_weights<<<G, 256, smw, s>>>(F, cdp.as<double>(), w.as<double>());
+    FitParams Fw = F;
+    Fw.w = w.as<double>();
+    DevBuf Rwb;
+    rc = tsqr(Fw, n, sms, &Rwb, s, err, errlen);
+    if (rc) return rc;
+    col_scale_from_R<<<1, 64, 0, s>>>(Rwb.as<double>(), n, Sw.as<double>());
+    int f2 = 0;
+    rc = minimizer(F, Rwb.as<double>(), Sw.as<double>(), gsum.as<double>(), refined.as<double>(),
+                   next.as<double>(), &f2, sms, s, err, errlen);
+    if (rc) return rc;
+    if (!f2) break;
+    FCUDA(cudaMemcpyAsync(refined.p, next.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  }
+  if (found) FCUDA(cudaMemcpyAsync(c, refined.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  FCUDA(cudaStreamSynchronize(s));
+  return RPG_OK;
+}
+
+extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int32_t n_vars,
+                                const int32_t* num_bounds, const int32_t* den_bounds,
+                                double rank_tol, int32_t device, double* coef_out,
+                                double* sigma_out, int32_t* rank_out, int32_t* truncated_out,
+                                double* residual_out, int32_t* safeguard_out, char* err,
+                                size_t errlen) {
+  if (m <= 0 || !X || !y) return fset_err(err, errlen, RPG_E_INVALID, "fit_rational: no samples");
+  if (n_vars < 1 || n_vars > RPG_MAX_VARS || !num_bounds || !den_bounds)
+    return fset_err(err, errlen, RPG_E_INVALID, "fit_rational: bad variable count");
+  for (int v = 0; v < n_vars; ++v)
+    if (num_bounds[v] < 0 || den_bounds[v] < 0)
+      return fset_err(err, errlen, RPG_E_INVALID, "negative degree bound");
+  const auto nb = basis(num_bounds, n_vars), db = basis(den_bounds, n_vars);
+  const int nn = (int)nb.size(), nd = (int)db.size(), n = nn + nd;
+  if (n > kMaxCols)
+    return fset_err(err, errlen, RPG_E_INVALID,
+                    "fit_rational: %d coefficients exceed the GPU fit's limit of %d", n, kMaxCols);
+  std::vector<uint8_t> exps((size_t)n * n_vars);
+  for (int k = 0; k < nn; ++k)
+    for (int v = 0; v < n_vars; ++v) exps[(size_t)k * n_vars + v] = (uint8_t)nb[k][v];
+  for (int k = 0; k < nd; ++k)
+    for (int v = 0; v < n_vars; ++v) exps[(size_t)(nn + k) * n_vars + v] = (uint8_t)db[k][v];
+
+  FCUDA(cudaSetDevice(device));
+  cudaStream_t s;
+  FCUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{s};
+  int sms = 148;
+  FCUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  DevBuf dX, dy, dexps, dR, dsig, dV, dscale, dc, dpart, dflags, dstats, dU;
+  FCUDA(cudaMalloc(&dX.p, sizeof(double) * (size_t)m * n_vars));
+  FCUDA(cudaMalloc(&dy.p, sizeof(double) * (size_t)m));
+  FCUDA(cudaMalloc(&dexps.p, exps.size()));
+  FCUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * (size_t)m * n_vars, cudaMemcpyHostToDevice, s));
+  FCUDA(cudaMemcpyAsync(dy.p, y, sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, s));
+  FCUDA(cudaMemcpyAsync(dexps.p, exps.data(), exps.size(), cudaMemcpyHostToDevice, s));
+  FCUDA(cudaMalloc(&dflags.p, sizeof(int) * 8));
+  FCUDA(cudaMemsetAsync(dflags.p, 0, sizeof(int) * 8, s));
+
+  FitParams F{};
+  F.n_vars = n_vars;
+  F.nn = nn;
+  F.nd = nd;
+  F.n = n;
+  F.X = dX.as<double>();
+  F.y = dy.as<double>();
+  F.w = nullptr;
+  F.exps = dexps.as<uint8_t>();
+  F.m = m;
+  int rc = tsqr(F, n, sms, &dR, s, err, errlen);
+  if (rc) return rc;
+  // Non-finite entries of A propagate into R (svd, polyfit.hpp:163).
+  all_finite<<<1, 256, 0, s>>>(dR.as<double>(), (int64_t)n * n, dflags.as<int>() + 4);
+  FCUDA(cudaMalloc(&dsig.p, sizeof(double) * n));
+  FCUDA(cudaMalloc(&dV.p, sizeof(double) * n * n));
+  FCUDA(cudaMalloc(&dscale.p, sizeof(double) * n));
+  FCUDA(cudaMalloc(&dc.p, sizeof(double) * n));
+  const size_t sm3 = sizeof(double) * (2 * (size_t)kMaxCols * kMaxCols + kMaxCols) + sizeof(int) * (kMaxCols + 4);
+  FCUDA(cudaFuncSetAttribute(svd_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
+  svd_small<<<1, kFitThreads, sm3, s>>>(dR.as<double>(), n, dsig.as<double>(), dV.as<double>(),
+                                        dscale.as<double>(), nullptr, 1);
+  FCUDA(cudaGetLastError());
+  smallest_vector<<<1, 64, 0, s>>>(dV.as<double>(), dscale.as<double>(), n, dc.as<double>());
+  // Safeguard trigger statistics.
+  const int G = std::max(1, std::min<int>((int)((m + 255) / 256), 4 * sms));
+  FCUDA(cudaMalloc(&dpart.p, sizeof(double) * 4 * G));
+  FCUDA(cudaMalloc(&dstats.p, sizeof(double) * 4));
+  const size_t sm4 = sizeof(double) * 32 + (size_t)kMaxCols * RPG_MAX_VARS + 16;
+  den_stats<<<G, 256, sm4, s>>>(F, dc.as<double>() + nn, dpart.as<double>());
+  den_stats_final<<<1, 32, 0, s>>>(dpart.as<double>(), G, m, dflags.as<int>() + 0,
+                                   dstats.as<double>());
+  int flags[8];
+  FCUDA(cudaMemcpyAsync(flags, dflags.p, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  FCUDA(cudaStreamSynchronize(s));
+  if (flags[4]) return fset_err(err, errlen, RPG_E_FIT, "svd: matrix has non-finite entries");
+  const int trigger = flags[0];
+  if (trigger) {
+    rc = rpg_fit_safeguard(F, dR.as<double>(), dscale.as<double>(), dc.as<double>(), rank_tol,
+                           sms, s, err, errlen);
+    if (rc) return rc;
+  }
+  const int nsig = (int)std::min<int64_t>(m, n);
+  fit_finalize<<<1, 32, 0, s>>>(dc.as<double>(), nn, nd, dsig.as<double>(), nsig, rank_tol,
+                                dflags.as<int>() + 1, dflags.as<int>() + 2);
+  FCUDA(cudaMemcpyAsync(flags, dflags.p, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  std::vector<double> sig(n);
+  FCUDA(cudaMemcpyAsync(sig.data(), dsig.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  if (coef_out)
+    FCUDA(cudaMemcpyAsync(coef_out, dc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  FCUDA(cudaStreamSynchronize(s));
+  if (flags[1] == 1) return fset_err(err, errlen, RPG_E_FIT, "all-zero coefficient vector");
+  if (flags[1] == 2)
+    return fset_err(err, errlen, RPG_E_FIT, "recovered denominator is identically zero");
+  if (sigma_out) std::copy(sig.begin(), sig.begin() + nsig, sigma_out);
+  if (rank_out) *rank_out = flags[2];
+  if (truncated_out) *truncated_out = flags[2] < n - 1;
+  if (residual_out) *residual_out = nsig >= n ? sig[n - 1] : 0.0;
+  if (safeguard_out) *safeguard_out = trigger;
+  return RPG_OK;
+}

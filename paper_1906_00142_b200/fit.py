@@ -1,0 +1,120 @@
+"""Python mirror of the reference's fit API over librpgpu.so's GPU fit.
+
+``fit_rational`` keeps the shape of ``poly::fit_rational`` (polyfit.hpp:
+337-427) — returns (RationalFunction, FitReport) — and ``fit_all_metrics``
+that of ``pipe::fit_all_metrics`` (pipeline.hpp:145-184).  All arithmetic
+runs in the K3 kernels (rpg_fit.cu); the host only packs arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import abi as A
+from . import formats as F
+
+K_DEFAULT_RANK_TOL = 1e-10
+
+
+class DegenerateFit(RuntimeError):
+    """poly::DegenerateFit (polyfit.hpp:32)."""
+
+
+class SvdFailure(RuntimeError):
+    """poly::SvdFailure (polyfit.hpp:35)."""
+
+
+class AllMetricsFailed(RuntimeError):
+    """pipe::AllMetricsFailed (pipeline.hpp:46)."""
+
+
+@dataclass
+class FitReport:
+    """poly::FitReport (polyfit.hpp:86-92) + whether the safeguard ran."""
+    residual_norm: float = 0.0
+    numerical_rank: int = 0
+    singular_values: List[float] = field(default_factory=list)
+    truncated: bool = False
+    holdout_relative_error: Optional[float] = None
+    safeguard: bool = False
+
+
+def fit_rational(X, y, variables: Sequence[str], num_bounds: Sequence[int],
+                 den_bounds: Sequence[int], rank_tol: float = K_DEFAULT_RANK_TOL,
+                 device: int = 0) -> Tuple[F.RationalFunction, FitReport]:
+    lib = A.load_library()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    if X.ndim == 1:
+        X = X[:, None]
+    y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
+    m, nv = X.shape if len(y) else (0, len(variables))
+    if len(y) != m:
+        raise F.ModelError("fit_rational: points/values size mismatch")
+    nb = F.monomial_basis(num_bounds)
+    db = F.monomial_basis(den_bounds)
+    n = len(nb) + len(db)
+    coef = np.zeros(n)
+    sig = np.zeros(max(1, min(m, n)))
+    rank, trunc, safe = C.c_int32(), C.c_int32(), C.c_int32()
+    resid = C.c_double()
+    nbnd = (C.c_int32 * nv)(*num_bounds)
+    dbnd = (C.c_int32 * nv)(*den_bounds)
+    err = C.create_string_buffer(512)
+    rc = lib.rpg_fit_rational(A.ptr(X, C.c_double) if m else None, A.ptr(y, C.c_double) if m else None,
+                              m, nv, nbnd, dbnd, rank_tol, device, A.ptr(coef, C.c_double),
+                              A.ptr(sig, C.c_double), C.byref(rank), C.byref(trunc),
+                              C.byref(resid), C.byref(safe), err, len(err))
+    if rc != A.RPG_OK:
+        msg = err.value.decode()
+        if rc == A.RPG_E_INVALID:
+            raise ValueError(msg)
+        if rc == A.RPG_E_FIT:
+            raise (SvdFailure if msg.startswith("svd") else DegenerateFit)(msg)
+        raise A.RpgError(rc, msg)
+    f = F.RationalFunction(F.Polynomial(list(variables), nb, list(coef[: len(nb)])),
+                           F.Polynomial(list(variables), db, list(coef[len(nb):])))
+    rep = FitReport(residual_norm=resid.value, numerical_rank=rank.value,
+                    singular_values=list(sig[: min(m, n)]), truncated=bool(trunc.value),
+                    safeguard=bool(safe.value))
+    return f, rep
+
+
+def default_bounds(n_variables: int) -> Tuple[List[int], List[int]]:
+    """pipe::default_bounds (pipeline.hpp:88-93)."""
+    return [2] * n_variables, [1] * n_variables
+
+
+def fit_all_metrics(X, metric_values: Dict[str, np.ndarray], variables: Sequence[str],
+                    bounds: Dict[str, Tuple[List[int], List[int]]],
+                    constants: Dict[str, float], rank_tol: float = K_DEFAULT_RANK_TOL,
+                    device: int = 0) -> F.MetricModelSet:
+    """pipe::fit_all_metrics (pipeline.hpp:145-184): one fit per metric
+    column; numerical failures are recorded per metric, a total wipeout
+    raises AllMetricsFailed."""
+    if len(X) == 0:
+        raise ValueError("fit_all_metrics: sample set is empty")
+    out = F.MetricModelSet(list(variables), {}, {}, dict(constants), {})
+    for metric in sorted(metric_values):
+        if metric in constants:
+            raise F.PipelineError(
+                f"metric '{metric}' is both a sample column and a declared constant")
+        nb, db = bounds.get(metric, default_bounds(len(variables)))
+        if len(nb) != len(variables) or len(db) != len(variables):
+            raise F.PipelineError(f"degree bounds for metric '{metric}' must have "
+                                  f"{len(variables)} entries per side")
+        try:
+            f, rep = fit_rational(X, metric_values[metric], variables, nb, db, rank_tol, device)
+            out.models[metric] = f
+            out.reports[metric] = {"residual_norm": rep.residual_norm,
+                                   "numerical_rank": rep.numerical_rank,
+                                   "truncated": rep.truncated,
+                                   "singular_values": rep.singular_values}
+        except (DegenerateFit, SvdFailure) as e:
+            out.failures[metric] = str(e)
+    if not out.models:
+        raise AllMetricsFailed("no metric could be fitted:" +
+                               "".join(f" [{k}: {v}]" for k, v in sorted(out.failures.items())))
+    return out
