@@ -147,8 +147,13 @@ def positive_den_minimizer(A_eq, col_scale, den_values, num_size, start_raw):
     for _outer in range(16):
         for _inner in range(40):
             qinv = 1.0 / q
-            grad = 2.0 * (H0 @ c) - mu * (Q.T @ qinv)
-            H = 2.0 * H0 + mu * (Q.T * (qinv ** 2)) @ Q
+            # Q is zero outside the denominator block: same algebra, den block only
+            Qd = Q[:, num_size: num_size + nd]
+            qt = np.zeros(n)
+            qt[num_size: num_size + nd] = Qd.T @ qinv
+            grad = 2.0 * (H0 @ c) - mu * qt
+            H = 2.0 * H0
+            H[num_size: num_size + nd, num_size: num_size + nd] += mu * (Qd.T * (qinv ** 2)) @ Qd
             K[:] = 0.0
             K[:n, :n] = H
             K[:n, n] = g
