@@ -220,10 +220,16 @@ def gpu_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:  # test mode: every rank on cuda:0 (multi-rank path on one GPU)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     dev = torch.device("cuda", local)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")  # collective buffers
 
     hw, specs, space = load_workload()
     opts = S.SearchOptions(arith=args.arith, kernel=args.kernel, device=local)
@@ -233,7 +239,7 @@ def gpu_arm(args):
     data_host = np.arange(lo, lo + n, dtype=np.int64).reshape(n, 1)
     data_dev = torch.from_numpy(data_host).to(dev)
     out_dev = {k: torch.empty(n * A.WINNER_DTYPE.itemsize, dtype=torch.uint8, device=dev) for k in KERNELS}
-    gathered = {k: torch.empty(world * n * A.WINNER_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    gathered = {k: torch.empty(world * n * A.WINNER_DTYPE.itemsize, dtype=torch.uint8, device=cdev)
                 for k in KERNELS} if world > 1 else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -245,7 +251,7 @@ def gpu_arm(args):
             plans[k].search_batch_device(data_dev.data_ptr(), n, 1, out_dev[k].data_ptr(), sptr)
         if world > 1:
             for k in KERNELS:
-                dist.all_gather_into_tensor(gathered[k], out_dev[k])
+                dist.all_gather_into_tensor(gathered[k], out_dev[k].to(cdev))
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -269,7 +275,7 @@ def gpu_arm(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    total_ms = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    total_ms = torch.tensor([sum(times)], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     total_ms = float(total_ms.item())
@@ -312,7 +318,7 @@ def gpu_arm(args):
         for k in KERNELS:
             e2e_out[k] = plans[k].search_batch(pinned_np)
         e2e_times.append(time.perf_counter() - t0)
-    e2e_total = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+    e2e_total = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(e2e_total, op=dist.ReduceOp.MAX)
     e2e_value = world * evals_per_rank_step * args.steps / float(e2e_total.item())
@@ -374,6 +380,9 @@ def main():
     ap.add_argument("--kernel", choices=["specialized", "generic"], default="specialized")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default) | gloo (test mode)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="test mode: all ranks on cuda:0 (with --dist-backend gloo)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)

@@ -19,7 +19,7 @@ struct Module {
 
 // CUDA source of the specialized kernels for a plan's model.
 std::string generate_source(const rpg::Params& P, const std::vector<double>& coef,
-                            const std::vector<uint64_t>& exps, bool fast);
+                            const std::vector<uint64_t>& exps, bool fast, bool two_point = false);
 
 // NVRTC -> sm_100a cubin.
 int compile(const std::string& source, int min_blocks, std::vector<char>* cubin,

@@ -591,7 +591,8 @@ extern "C" int64_t rpg_emit_cuda_source(const rpg_model* model, const rpg_profil
   int rc = prepare_model(model, hw, opts, P, tab, err, errlen);
   if (rc) return rc;
   const std::string src =
-      rpg_jit::generate_source(P, tab.coef, tab.exps, opts->arith == RPG_ARITH_FAST);
+      rpg_jit::generate_source(P, tab.coef, tab.exps, opts->arith == RPG_ARITH_FAST,
+                               getenv("RPG_JIT_ILP") && atoi(getenv("RPG_JIT_ILP")) == 2);
   if (buf && buflen) {
     const size_t n = std::min(buflen - 1, src.size());
     memcpy(buf, src.data(), n);
