@@ -26,7 +26,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -1153,8 +1155,21 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
   F.w = nullptr;
   F.exps = dexps.as<uint8_t>();
   F.m = m;
+  // RPG_FIT_TRACE=1: per-phase wall times on stderr (profiling aid).
+  const bool trace = getenv("RPG_FIT_TRACE") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[rpg_fit] %-12s %9.3f ms\n", name,
+            std::chrono::duration<double, std::milli>(now - t_prev).count());
+    t_prev = now;
+  };
+  phase("upload");
   int rc = tsqr(F, n, sms, &dR, s, err, errlen);
   if (rc) return rc;
+  phase("tsqr");
   // Non-finite entries of A propagate into R (svd, polyfit.hpp:163).
   all_finite<<<1, 256, 0, s>>>(dR.as<double>(), (int64_t)n * n, dflags.as<int>() + 4);
   FCUDA(cudaMalloc(&dsig.p, sizeof(double) * n));
@@ -1180,10 +1195,12 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
   FCUDA(cudaStreamSynchronize(s));
   if (flags[4]) return fset_err(err, errlen, RPG_E_FIT, "svd: matrix has non-finite entries");
   const int trigger = flags[0];
+  phase("svd+stats");
   if (trigger) {
     rc = rpg_fit_safeguard(F, dR.as<double>(), dscale.as<double>(), dc.as<double>(), rank_tol,
                            sms, s, err, errlen);
     if (rc) return rc;
+    phase("safeguard");
   }
   const int nsig = (int)std::min<int64_t>(m, n);
   fit_finalize<<<1, 32, 0, s>>>(dc.as<double>(), nn, nd, dsig.as<double>(), nsig, rank_tol,

@@ -45,7 +45,10 @@ def main():
         ys[name] = np.ascontiguousarray(y)
     nb, db = [2, 2, 2], [1, 1, 1]
     # warm-up (context, module load)
-    G.fit_rational(X[:4096], ys[F.METRIC_COMP][:4096], spec.variables, nb, db)
+    try:
+        G.fit_rational(X[:4096], ys[F.METRIC_COMP][:4096], spec.variables, nb, db)
+    except (G.DegenerateFit, G.SvdFailure):
+        pass
     times, safeguards = [], {}
     for _ in range(args.reps):
         t0 = time.perf_counter()
