@@ -98,7 +98,8 @@ enum {
   RPG_E_CUDA = -4,         /* device / driver failure */
   RPG_E_NO_FEASIBLE = -5,  /* pipe::NoFeasibleConfig (single-tuple calls) */
   RPG_E_PIPELINE = -6,     /* pipe::PipelineError */
-  RPG_E_FIT = -7           /* poly::DegenerateFit / SvdFailure */
+  RPG_E_FIT = -7,          /* poly::DegenerateFit / SvdFailure */
+  RPG_E_EVAL = -8          /* ir::EvalError / DivisionByZero (bare programs) */
 };
 
 /* perf::DeviceProfile, same fields and order (perfmodel.hpp:50-65). */
@@ -237,6 +238,62 @@ int rpg_fit_rational(const double* X, const double* y, int64_t m, int32_t n_vars
                      double* sigma_out, int32_t* rank_out, int32_t* truncated_out,
                      double* residual_out, int32_t* safeguard_out, char* err,
                      size_t errlen);
+
+/* A bare rational program (ir::RationalProgram, ir.hpp:19-112) lowered for
+ * the GPU: variables are slots, literals are doubles (to_double of each
+ * rational, as the reference's C lowering prints them, pipeline.hpp:276-433).
+ * op: ir::Opcode order (assign, neg, add, sub, mul, euclid_quot, euclid_rem,
+ * floor_div, ceil_div, cmp_eq, cmp_lt, branch_if, jump, halt_return).
+ * Operands a/b: slot index >= 0, or literal -1-k.  t0/t1: jump targets. */
+typedef struct {
+  int32_t op, target, a, b, t0, t1;
+} rpg_instr;
+
+#define RPG_INPUT_FIXED (-100)
+
+typedef struct {
+  int32_t n_instr, n_slots, n_literals, output_slot;
+  const rpg_instr* body;
+  const double* literals;
+  int32_t n_inputs;
+  int32_t reserved;
+  const int32_t* input_slot;  /* slot of each declared input */
+  const int32_t* input_kind;  /* RPG_VAR_BX/BY/BZ, data index >= 0, RPG_INPUT_FIXED */
+  const double* input_fixed;  /* value of RPG_INPUT_FIXED inputs (profile fields) */
+  int64_t step_limit;         /* interp.hpp:31 (1e6) */
+} rpg_program;
+
+/* pipe::search_optimal for a bare program (no metric spec; the `--rp`
+ * path, ratprog_cli.cpp:305-307): Ec = the program's value (evaluated with
+ * the reference C lowering's double semantics on the GPU), feasible iff >= 0,
+ * occupancy from opts->regs_per_thread / shared_words_per_block
+ * (pipeline.hpp:648-650), case tag "-".  The returned plan works with
+ * rpg_search_batch / rpg_evaluate and their _device variants; evaluation
+ * errors (zero divisor, step limit, control falling off the end, reading an
+ * unassigned variable — the exact interpreter's throws, interp.hpp:44-121)
+ * fail the host-buffer calls with RPG_E_EVAL (see rpg_plan_poll_error for
+ * the _device calls).  Inputs bind as make_binding_plan does
+ * (pipeline.hpp:482-516): bx/by/bz per configuration, D<k> from the data
+ * tuple, device-profile fields fixed (input_fixed). */
+int rpg_program_plan_create(const rpg_program* prog, const rpg_profile* hw,
+                            const rpg_config* space, int64_t n_space,
+                            const rpg_options* opts, int32_t device,
+                            rpg_plan** out, char* err, size_t errlen);
+
+/* The CUDA source of the kernels rpg_program_plan_create compiles for a
+ * bare program (the counterpart of pipe::emit_c_source, pipeline.hpp:
+ * 276-433); same buffer / compile / return conventions as
+ * rpg_emit_cuda_source. */
+int64_t rpg_emit_program_cuda_source(const rpg_program* prog, const rpg_profile* hw,
+                                     const rpg_options* opts, int32_t compile, char* buf,
+                                     size_t buflen, int64_t* cubin_bytes, char* err,
+                                     size_t errlen);
+
+/* Errors of _device calls on a bare-program plan: synchronizes `stream`
+ * (may be NULL), then returns and clears the first evaluation error recorded
+ * since the last check (RPG_E_EVAL with the interpreter's message and the
+ * failing tuple/configuration), or RPG_OK.  No-op for metric-spec plans. */
+int rpg_plan_poll_error(rpg_plan* plan, void* stream, char* err, size_t errlen);
 
 /* One-shot convenience for FFI callers. */
 int rpg_search(const rpg_model* model, const rpg_profile* hw,

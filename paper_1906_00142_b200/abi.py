@@ -33,6 +33,7 @@ RPG_E_CUDA = -4
 RPG_E_NO_FEASIBLE = -5
 RPG_E_PIPELINE = -6
 RPG_E_FIT = -7
+RPG_E_EVAL = -8
 
 
 class rpg_profile(C.Structure):
@@ -204,6 +205,15 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                        C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32), C.POINTER(C.c_double),
                                        C.POINTER(C.c_int32)) + errbuf),
+        "rpg_program_plan_create": (C.c_int, (C.c_void_p, C.POINTER(rpg_profile),
+                                              C.POINTER(rpg_config), C.c_int64,
+                                              C.POINTER(rpg_options), C.c_int32,
+                                              C.POINTER(C.c_void_p)) + errbuf),
+        "rpg_plan_poll_error": (C.c_int, (C.c_void_p, C.c_void_p) + errbuf),
+        "rpg_emit_program_cuda_source": (C.c_int64, (C.c_void_p, C.POINTER(rpg_profile),
+                                                     C.POINTER(rpg_options), C.c_int32,
+                                                     C.c_char_p, C.c_size_t,
+                                                     C.POINTER(C.c_int64)) + errbuf),
         "rpg_search": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
                                  C.POINTER(rpg_config), C.c_int64,
                                  C.POINTER(rpg_options), C.POINTER(C.c_int64),
@@ -221,7 +231,8 @@ EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_plan_destroy", "rpg_search_batch",
                     "rpg_search_batch_device", "rpg_evaluate",
                     "rpg_evaluate_device", "rpg_search", "rpg_emit_cuda_source",
-                    "rpg_fit_rational")
+                    "rpg_fit_rational", "rpg_program_plan_create",
+                    "rpg_plan_poll_error", "rpg_emit_program_cuda_source")
 
 
 class RpgError(RuntimeError):

@@ -30,4 +30,11 @@ int get_module(const rpg::Params& P, const std::vector<double>& coef,
                const std::vector<uint64_t>& exps, bool fast, int device, int min_blocks,
                Module* out, std::string* err);
 
+// Same, for an already generated source.
+int get_module_src(const std::string& src, int device, int min_blocks, Module* out,
+                   std::string* err);
+
+// Specialized kernels for a bare rational program (rpg_program.cu).
+std::string generate_program_source(const rpg_program& prog, const rpg::Params& P);
+
 }  // namespace rpg_jit

@@ -122,6 +122,10 @@ struct rpg_plan {
   int32_t* d_slot_terms = nullptr;
   int4* d_cfg = nullptr;
   int4* d_occ = nullptr;
+  // bare-program plans: first evaluation error (Params::err_flag)
+  bool is_program = false;
+  long long step_limit = 0;
+  unsigned long long* d_err = nullptr;
   // host-API staging
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -304,6 +308,227 @@ int prepare_model(const rpg_model* model, const rpg_profile* hw, const rpg_optio
   return RPG_OK;
 }
 
+int check_space(const rpg_config* space, int64_t n_space, char* err, size_t errlen) {
+  if (n_space <= 0 || !space)
+    return set_err(err, errlen, RPG_E_INVALID, "search_optimal: configuration space is empty");
+  if (n_space > (int64_t)0x7ffffff0)
+    return set_err(err, errlen, RPG_E_INVALID, "configuration space too large");
+  for (int64_t i = 0; i < n_space; ++i) {
+    const rpg_config& c = space[i];
+    if (c.bx < INT32_MIN || c.bx > INT32_MAX || c.by < INT32_MIN || c.by > INT32_MAX ||
+        c.bz < INT32_MIN || c.bz > INT32_MAX)
+      return set_err(err, errlen, RPG_E_INVALID, "block dimension out of int32 range");
+  }
+  return RPG_OK;
+}
+
+// Shared tail of plan creation: configuration table {bx, by, bz, lex rank},
+// term tables, occupancy table, kernels (`jit` loads the specialized module)
+// and launch geometry.
+template <class Jit>
+int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64_t n_space,
+               int32_t device, bool fast, bool specialized, bool is_program, const Jit& jit,
+               rpg_plan** out, char* err, size_t errlen) {
+  const std::vector<double>& coef = tab.coef;
+  const std::vector<uint64_t>& exps = tab.exps;
+  const std::vector<int32_t>& slot_begin = tab.slot_begin;
+  const std::vector<int32_t>& slot_terms = tab.slot_terms;
+
+  std::vector<int4> cfg((size_t)n_space);
+  std::vector<int32_t> order((size_t)n_space);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    const rpg_config &x = space[a], &y = space[b];
+    if (x.bx != y.bx) return x.bx < y.bx;
+    if (x.by != y.by) return x.by < y.by;
+    return x.bz < y.bz;
+  });
+  for (int64_t r = 0; r < n_space; ++r) {
+    const int32_t i = order[r];
+    cfg[i] = make_int4((int)space[i].bx, (int)space[i].by, (int)space[i].bz, (int)r);
+  }
+
+  rpg_plan* plan = new rpg_plan();
+  plan->device = device;
+  plan->max_data_index = tab.max_d;
+  plan->fast = fast;
+  plan->specialized = specialized;
+  plan->is_program = is_program;
+  auto fail = [&](int code) {
+    rpg_plan_destroy(plan);
+    return code;
+  };
+#define PLAN_CUDA(expr)                                                          \
+  do {                                                                           \
+    cudaError_t e_ = (expr);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      return fail(set_err(err, errlen, RPG_E_CUDA, "%s: %s", #expr,              \
+                          cudaGetErrorString(e_)));                              \
+  } while (0)
+  PLAN_CUDA(cudaSetDevice(device));
+  PLAN_CUDA(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+  PLAN_CUDA(cudaDeviceGetAttribute(&plan->sm_count, cudaDevAttrMultiProcessorCount, device));
+  const size_t nt = std::max<size_t>(coef.size(), 1);
+  PLAN_CUDA(cudaMalloc(&plan->d_coef, sizeof(double) * nt));
+  PLAN_CUDA(cudaMalloc(&plan->d_exps, sizeof(uint64_t) * nt));
+  PLAN_CUDA(cudaMalloc(&plan->d_slot_begin, sizeof(int32_t) * slot_begin.size()));
+  PLAN_CUDA(cudaMalloc(&plan->d_slot_terms, sizeof(int32_t) * std::max<size_t>(slot_terms.size(), 1)));
+  PLAN_CUDA(cudaMalloc(&plan->d_cfg, sizeof(int4) * cfg.size()));
+  PLAN_CUDA(cudaMalloc(&plan->d_occ, sizeof(int4) * cfg.size()));
+  PLAN_CUDA(cudaMalloc(&plan->d_err, sizeof(unsigned long long)));
+  PLAN_CUDA(cudaMemset(plan->d_err, 0xff, sizeof(unsigned long long)));
+  if (!coef.empty()) {
+    PLAN_CUDA(cudaMemcpy(plan->d_coef, coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice));
+    PLAN_CUDA(cudaMemcpy(plan->d_exps, exps.data(), sizeof(uint64_t) * exps.size(), cudaMemcpyHostToDevice));
+  }
+  PLAN_CUDA(cudaMemcpy(plan->d_slot_begin, slot_begin.data(), sizeof(int32_t) * slot_begin.size(), cudaMemcpyHostToDevice));
+  if (!slot_terms.empty())
+    PLAN_CUDA(cudaMemcpy(plan->d_slot_terms, slot_terms.data(), sizeof(int32_t) * slot_terms.size(), cudaMemcpyHostToDevice));
+  PLAN_CUDA(cudaMemcpy(plan->d_cfg, cfg.data(), sizeof(int4) * cfg.size(), cudaMemcpyHostToDevice));
+  P.coef = plan->d_coef;
+  P.exps = plan->d_exps;
+  P.slot_begin = plan->d_slot_begin;
+  P.slot_terms = plan->d_slot_terms;
+  P.cfg = plan->d_cfg;
+  P.n_space = (int32_t)n_space;
+  P.occ = plan->d_occ;
+  P.err_flag = plan->d_err;
+  P.d = 0;
+  if (P.occ_const) {
+    occ_table_kernel<<<(int)((n_space + 255) / 256), 256, 0, plan->stream>>>(P, plan->d_occ);
+    PLAN_CUDA(cudaGetLastError());
+    PLAN_CUDA(cudaStreamSynchronize(plan->stream));
+  }
+
+  plan->smem = smem_layout(P.n_terms, P.n_slots).total;
+  int smem_optin = 0;
+  PLAN_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  if (plan->smem > (size_t)smem_optin)
+    return fail(set_err(err, errlen, RPG_E_MODEL, "model too large for shared memory"));
+  if (plan->specialized) {
+    std::string jerr;
+    // Resident CTAs per SM the specialized kernels are register-budgeted for
+    // (launch bounds); RPG_JIT_MIN_BLOCKS overrides it for tuning sweeps.
+    int min_blocks = 3;
+    if (const char* e = getenv("RPG_JIT_MIN_BLOCKS")) min_blocks = std::max(1, atoi(e));
+    if (jit(min_blocks, &plan->jit, &jerr) != 0)
+      return fail(set_err(err, errlen, RPG_E_CUDA, "%s", jerr.c_str()));
+  }
+  auto setup = [&](const void* fn, int* grid) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)plan->smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, plan->smem);
+    if (e != cudaSuccess) return e;
+    *grid = std::max(1, per_sm) * plan->sm_count;
+    return cudaSuccess;
+  };
+  PLAN_CUDA(setup(search_fn(plan), &plan->grid_search));
+  PLAN_CUDA(setup(evaluate_fn(plan), &plan->grid_eval));
+  plan->P = P;
+#undef PLAN_CUDA
+  *out = plan;
+  return RPG_OK;
+}
+
+// Validates a bare program (include/rpg.h rpg_program) and builds its Params:
+// no metric tables; the occupancy context of every row is opts regs/shared
+// (pipeline.hpp:648-650), served by the constant-metric occupancy table.
+int prepare_program(const rpg_program* prog, const rpg_profile* hw, const rpg_options* opts,
+                    Params& P, ModelTables& tab, char* err, size_t errlen) {
+  int rc = validate_profile(hw, err, errlen);
+  if (rc) return rc;
+  if (opts->rep_mode != RPG_REP_REAL && opts->rep_mode != RPG_REP_CEIL)
+    return set_err(err, errlen, RPG_E_INVALID, "rep_mode must be real or ceil");
+  if (prog->step_limit < 1)
+    return set_err(err, errlen, RPG_E_INVALID, "step_limit must be >= 1");
+  if (prog->n_instr < 1 || !prog->body)
+    return set_err(err, errlen, RPG_E_INVALID, "empty program body");
+  if (prog->n_slots < 1 || prog->n_slots > (1 << 20) || prog->n_literals < 0 ||
+      (prog->n_literals > 0 && !prog->literals) || prog->n_inputs < 0 ||
+      (prog->n_inputs > 0 && (!prog->input_slot || !prog->input_kind || !prog->input_fixed)))
+    return set_err(err, errlen, RPG_E_INVALID, "malformed rpg_program");
+  if (prog->output_slot < 0 || prog->output_slot >= prog->n_slots)
+    return set_err(err, errlen, RPG_E_INVALID, "malformed rpg_program: output slot");
+  for (int i = 0; i < prog->n_inputs; ++i) {
+    const int s = prog->input_slot[i], k = prog->input_kind[i];
+    if (s < 0 || s >= prog->n_slots)
+      return set_err(err, errlen, RPG_E_INVALID, "malformed rpg_program: input slot");
+    if (k >= kMaxData)
+      return set_err(err, errlen, RPG_E_PIPELINE, "program input 'D%d' out of range", k + 1);
+    if (k != RPG_VAR_BX && k != RPG_VAR_BY && k != RPG_VAR_BZ && k != RPG_INPUT_FIXED && k < 0)
+      return set_err(err, errlen, RPG_E_INVALID, "malformed rpg_program: input kind %d", k);
+    if (k == RPG_INPUT_FIXED && !std::isfinite(prog->input_fixed[i]))
+      return set_err(err, errlen, RPG_E_INVALID, "malformed rpg_program: input value");
+    if (k >= 0) tab.max_d = std::max(tab.max_d, k);
+  }
+  for (int i = 0; i < prog->n_instr; ++i) {
+    const rpg_instr& in = prog->body[i];
+    if (in.op < 0 || in.op > 13)
+      return set_err(err, errlen, RPG_E_INVALID, "malformed rpg_program: opcode at %d", i);
+    const int nops = (in.op == 0 || in.op == 1 || in.op == 11 || in.op == 13) ? 1
+                     : in.op == 12                                          ? 0
+                                                                            : 2;
+    const int ops[2] = {in.a, in.b};
+    for (int k = 0; k < nops; ++k)
+      if (ops[k] >= prog->n_slots || (ops[k] < 0 && -1 - ops[k] >= prog->n_literals))
+        return set_err(err, errlen, RPG_E_INVALID, "malformed rpg_program: operand at %d", i);
+    if (in.op <= 10 && (in.target < 0 || in.target >= prog->n_slots))
+      return set_err(err, errlen, RPG_E_INVALID, "malformed rpg_program: target at %d", i);
+  }
+  for (int i = 0; i < prog->n_literals; ++i)
+    if (!std::isfinite(prog->literals[i]))
+      return set_err(err, errlen, RPG_E_INVALID, "program literal %d is not finite as a double", i);
+
+  P = Params{};
+  P.hw = *hw;
+  hoist_hardware(P);
+  P.rep_mode = opts->rep_mode;
+  P.arith = RPG_ARITH_EXACT;
+  P.tie_rel_tol = opts->tie_rel_tol;
+  P.fb_regs = opts->regs_per_thread;
+  P.fb_shared = opts->shared_words_per_block;
+  P.n_vars = 0;
+  for (int i = 0; i < prog->n_inputs; ++i)
+    if (prog->input_kind[i] == RPG_VAR_BZ) P.has_bz = 1;
+  for (int s = 0; s < RPG_N_METRICS; ++s) P.metric[s].is_const = 1;
+  P.metric[RPG_METRIC_REGS].value = opts->regs_per_thread;
+  P.metric[RPG_METRIC_SHARED].value = opts->shared_words_per_block;
+  P.occ_const = 1;
+  return RPG_OK;
+}
+
+// Reads and clears a program plan's error word (plan->mu held, stream idle).
+int take_program_error(rpg_plan* plan, char* err, size_t errlen) {
+  unsigned long long key = ~0ull;
+  CUDA_TRY(cudaMemcpy(&key, plan->d_err, sizeof(key), cudaMemcpyDeviceToHost));
+  if (key == ~0ull) return RPG_OK;
+  CUDA_TRY(cudaMemset(plan->d_err, 0xff, sizeof(key)));
+  const unsigned long long point = key >> 24;
+  const long long t = (long long)(point / (unsigned long long)plan->P.n_space);
+  const int c = (int)(point % (unsigned long long)plan->P.n_space);
+  const int kind = (int)(key & 15), detail = (int)((key >> 4) & 0xfffff);
+  char what[160];
+  switch (kind) {
+    case kProgErrFloorDiv: snprintf(what, sizeof(what), "floor_div: zero divisor"); break;
+    case kProgErrCeilDiv: snprintf(what, sizeof(what), "ceil_div: zero divisor"); break;
+    case kProgErrEuclidQuot: snprintf(what, sizeof(what), "euclid_quot: zero divisor"); break;
+    case kProgErrEuclidRem: snprintf(what, sizeof(what), "euclid_rem: zero divisor"); break;
+    case kProgErrStepLimit:
+      snprintf(what, sizeof(what),
+               "step limit of %lld instructions exceeded (possible non-termination)",
+               (long long)plan->step_limit);
+      break;
+    case kProgErrFellOff: snprintf(what, sizeof(what), "control fell off the end of the program"); break;
+    case kProgErrMissing:
+      snprintf(what, sizeof(what), "no value bound for variable slot %d", detail);
+      break;
+    default: snprintf(what, sizeof(what), "program evaluation failed (code %d)", kind); break;
+  }
+  return set_err(err, errlen, RPG_E_EVAL, "%s [tuple %lld, configuration %d]", what, t, c);
+}
+
 }  // namespace
 
 extern "C" {
@@ -326,6 +551,7 @@ int rpg_plan_destroy(rpg_plan* plan) {
   cudaFree(plan->d_slot_terms);
   cudaFree(plan->d_cfg);
   cudaFree(plan->d_occ);
+  cudaFree(plan->d_err);
   cudaFree(plan->d_data);
   cudaFree(plan->d_out);
   if (plan->stream) cudaStreamDestroy(plan->stream);
@@ -339,120 +565,52 @@ int rpg_plan_create(const rpg_model* model, const rpg_profile* hw, const rpg_con
   if (!model || !hw || !opts || !out)
     return set_err(err, errlen, RPG_E_INVALID, "rpg_plan_create: null argument");
   *out = nullptr;
-  if (n_space <= 0 || !space)
-    return set_err(err, errlen, RPG_E_INVALID, "search_optimal: configuration space is empty");
-  if (n_space > (int64_t)0x7ffffff0)
-    return set_err(err, errlen, RPG_E_INVALID, "configuration space too large");
   Params P;
   ModelTables tab;
-  int rc = prepare_model(model, hw, opts, P, tab, err, errlen);
+  int rc = check_space(space, n_space, err, errlen);
   if (rc) return rc;
-  const std::vector<double>& coef = tab.coef;
-  const std::vector<uint64_t>& exps = tab.exps;
-  const std::vector<int32_t>& slot_begin = tab.slot_begin;
-  const std::vector<int32_t>& slot_terms = tab.slot_terms;
-  const int max_d = tab.max_d;
+  rc = prepare_model(model, hw, opts, P, tab, err, errlen);
+  if (rc) return rc;
+  const bool fast = P.arith == RPG_ARITH_FAST;
+  return build_plan(P, tab, space, n_space, device, fast,
+                    opts->kernel == RPG_KERNEL_SPECIALIZED, false,
+                    [&](int min_blocks, rpg_jit::Module* m, std::string* jerr) {
+                      return rpg_jit::get_module(P, tab.coef, tab.exps, fast, device,
+                                                 min_blocks, m, jerr);
+                    },
+                    out, err, errlen);
+}
 
-  // Configuration table {bx, by, bz, lex rank}.
-  std::vector<int4> cfg((size_t)n_space);
-  std::vector<int32_t> order((size_t)n_space);
-  std::iota(order.begin(), order.end(), 0);
-  for (int64_t i = 0; i < n_space; ++i) {
-    const rpg_config& c = space[i];
-    if (c.bx < INT32_MIN || c.bx > INT32_MAX || c.by < INT32_MIN || c.by > INT32_MAX ||
-        c.bz < INT32_MIN || c.bz > INT32_MAX)
-      return set_err(err, errlen, RPG_E_INVALID, "block dimension out of int32 range");
-  }
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-    const rpg_config &x = space[a], &y = space[b];
-    if (x.bx != y.bx) return x.bx < y.bx;
-    if (x.by != y.by) return x.by < y.by;
-    return x.bz < y.bz;
-  });
-  for (int64_t r = 0; r < n_space; ++r) {
-    const int32_t i = order[r];
-    cfg[i] = make_int4((int)space[i].bx, (int)space[i].by, (int)space[i].bz, (int)r);
-  }
+int rpg_program_plan_create(const rpg_program* prog, const rpg_profile* hw,
+                            const rpg_config* space, int64_t n_space, const rpg_options* opts,
+                            int32_t device, rpg_plan** out, char* err, size_t errlen) {
+  if (!prog || !hw || !opts || !out)
+    return set_err(err, errlen, RPG_E_INVALID, "rpg_program_plan_create: null argument");
+  *out = nullptr;
+  int rc = check_space(space, n_space, err, errlen);
+  if (rc) return rc;
+  Params P;
+  ModelTables tab;
+  if ((rc = prepare_program(prog, hw, opts, P, tab, err, errlen))) return rc;
+  const rpg_program prog_copy = *prog;
+  rc = build_plan(P, tab, space, n_space, device, false, true, true,
+                  [&](int min_blocks, rpg_jit::Module* m, std::string* jerr) {
+                    return rpg_jit::get_module_src(
+                        rpg_jit::generate_program_source(prog_copy, P), device, min_blocks,
+                        m, jerr);
+                  },
+                  out, err, errlen);
+  if (rc == RPG_OK) (*out)->step_limit = prog->step_limit;
+  return rc;
+}
 
-  rpg_plan* plan = new rpg_plan();
-  plan->device = device;
-  plan->max_data_index = max_d;
-  plan->fast = P.arith == RPG_ARITH_FAST;
-  plan->specialized = opts->kernel == RPG_KERNEL_SPECIALIZED;
-  auto fail = [&](int code) {
-    rpg_plan_destroy(plan);
-    return code;
-  };
-#define PLAN_CUDA(expr)                                                          \
-  do {                                                                           \
-    cudaError_t e_ = (expr);                                                     \
-    if (e_ != cudaSuccess)                                                       \
-      return fail(set_err(err, errlen, RPG_E_CUDA, "%s: %s", #expr,              \
-                          cudaGetErrorString(e_)));                              \
-  } while (0)
-  PLAN_CUDA(cudaSetDevice(device));
-  PLAN_CUDA(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
-  PLAN_CUDA(cudaDeviceGetAttribute(&plan->sm_count, cudaDevAttrMultiProcessorCount, device));
-  const size_t nt = std::max<size_t>(coef.size(), 1);
-  PLAN_CUDA(cudaMalloc(&plan->d_coef, sizeof(double) * nt));
-  PLAN_CUDA(cudaMalloc(&plan->d_exps, sizeof(uint64_t) * nt));
-  PLAN_CUDA(cudaMalloc(&plan->d_slot_begin, sizeof(int32_t) * slot_begin.size()));
-  PLAN_CUDA(cudaMalloc(&plan->d_slot_terms, sizeof(int32_t) * std::max<size_t>(slot_terms.size(), 1)));
-  PLAN_CUDA(cudaMalloc(&plan->d_cfg, sizeof(int4) * cfg.size()));
-  PLAN_CUDA(cudaMalloc(&plan->d_occ, sizeof(int4) * cfg.size()));
-  if (!coef.empty()) {
-    PLAN_CUDA(cudaMemcpy(plan->d_coef, coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice));
-    PLAN_CUDA(cudaMemcpy(plan->d_exps, exps.data(), sizeof(uint64_t) * exps.size(), cudaMemcpyHostToDevice));
-  }
-  PLAN_CUDA(cudaMemcpy(plan->d_slot_begin, slot_begin.data(), sizeof(int32_t) * slot_begin.size(), cudaMemcpyHostToDevice));
-  if (!slot_terms.empty())
-    PLAN_CUDA(cudaMemcpy(plan->d_slot_terms, slot_terms.data(), sizeof(int32_t) * slot_terms.size(), cudaMemcpyHostToDevice));
-  PLAN_CUDA(cudaMemcpy(plan->d_cfg, cfg.data(), sizeof(int4) * cfg.size(), cudaMemcpyHostToDevice));
-  P.coef = plan->d_coef;
-  P.exps = plan->d_exps;
-  P.slot_begin = plan->d_slot_begin;
-  P.slot_terms = plan->d_slot_terms;
-  P.cfg = plan->d_cfg;
-  P.n_space = (int32_t)n_space;
-  P.occ = plan->d_occ;
-  P.d = 0;
-  if (P.occ_const) {
-    occ_table_kernel<<<(int)((n_space + 255) / 256), 256, 0, plan->stream>>>(P, plan->d_occ);
-    PLAN_CUDA(cudaGetLastError());
-    PLAN_CUDA(cudaStreamSynchronize(plan->stream));
-  }
-
-  // Kernels and launch geometry.
-  plan->smem = smem_layout(P.n_terms, P.n_slots).total;
-  int smem_optin = 0;
-  PLAN_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-  if (plan->smem > (size_t)smem_optin)
-    return fail(set_err(err, errlen, RPG_E_MODEL, "model too large for shared memory"));
-  if (plan->specialized) {
-    std::string jerr;
-    // Resident CTAs per SM the specialized kernels are register-budgeted for
-    // (launch bounds); RPG_JIT_MIN_BLOCKS overrides it for tuning sweeps.
-    int min_blocks = 3;
-    if (const char* e = getenv("RPG_JIT_MIN_BLOCKS")) min_blocks = std::max(1, atoi(e));
-    if (rpg_jit::get_module(P, coef, exps, plan->fast, device, min_blocks, &plan->jit, &jerr) != 0)
-      return fail(set_err(err, errlen, RPG_E_CUDA, "%s", jerr.c_str()));
-  }
-  auto setup = [&](const void* fn, int* grid) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)plan->smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, plan->smem);
-    if (e != cudaSuccess) return e;
-    *grid = std::max(1, per_sm) * plan->sm_count;
-    return cudaSuccess;
-  };
-  PLAN_CUDA(setup(search_fn(plan), &plan->grid_search));
-  PLAN_CUDA(setup(evaluate_fn(plan), &plan->grid_eval));
-  plan->P = P;
-#undef PLAN_CUDA
-  *out = plan;
-  return RPG_OK;
+int rpg_plan_poll_error(rpg_plan* plan, void* stream, char* err, size_t errlen) {
+  if (!plan) return set_err(err, errlen, RPG_E_INVALID, "null plan");
+  if (!plan->is_program) return RPG_OK;
+  std::lock_guard<std::mutex> lock(plan->mu);
+  CUDA_TRY(cudaSetDevice(plan->device));
+  if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return take_program_error(plan, err, errlen);
 }
 
 }  // extern "C"
@@ -519,12 +677,14 @@ int rpg_search_batch(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int3
   if (d > 0)
     CUDA_TRY(cudaMemcpyAsync(plan->d_data, data, sizeof(int64_t) * (size_t)n_tuples * d,
                              cudaMemcpyHostToDevice, plan->stream));
+  if (plan->is_program)
+    CUDA_TRY(cudaMemsetAsync(plan->d_err, 0xff, sizeof(unsigned long long), plan->stream));
   rc = launch_search(plan, plan->d_data, n_tuples, d, (rpg_winner*)plan->d_out, plan->stream,
                      err, errlen);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(out, plan->d_out, out_bytes, cudaMemcpyDeviceToHost, plan->stream));
   CUDA_TRY(cudaStreamSynchronize(plan->stream));
-  return RPG_OK;
+  return plan->is_program ? take_program_error(plan, err, errlen) : RPG_OK;
 }
 
 int rpg_evaluate_device(rpg_plan* plan, const int64_t* d_data, int64_t n_tuples, int32_t d,
@@ -557,6 +717,8 @@ int rpg_evaluate(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int32_t 
   if (d > 0)
     CUDA_TRY(cudaMemcpyAsync(plan->d_data, data, sizeof(int64_t) * (size_t)n_tuples * d,
                              cudaMemcpyHostToDevice, plan->stream));
+  if (plan->is_program)
+    CUDA_TRY(cudaMemsetAsync(plan->d_err, 0xff, sizeof(unsigned long long), plan->stream));
   rc = launch_evaluate(plan, plan->d_data, n_tuples, d, ec ? d_ec : nullptr,
                        tag ? d_tag : nullptr, wocc ? d_wocc : nullptr, plan->stream, err, errlen);
   if (rc) return rc;
@@ -564,7 +726,7 @@ int rpg_evaluate(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int32_t 
   if (wocc) CUDA_TRY(cudaMemcpyAsync(wocc, d_wocc, npts * sizeof(int32_t), cudaMemcpyDeviceToHost, plan->stream));
   if (tag) CUDA_TRY(cudaMemcpyAsync(tag, d_tag, npts, cudaMemcpyDeviceToHost, plan->stream));
   CUDA_TRY(cudaStreamSynchronize(plan->stream));
-  return RPG_OK;
+  return plan->is_program ? take_program_error(plan, err, errlen) : RPG_OK;
 }
 
 int rpg_search(const rpg_model* model, const rpg_profile* hw, const rpg_config* space,
@@ -593,6 +755,32 @@ extern "C" int64_t rpg_emit_cuda_source(const rpg_model* model, const rpg_profil
   const std::string src =
       rpg_jit::generate_source(P, tab.coef, tab.exps, opts->arith == RPG_ARITH_FAST,
                                getenv("RPG_JIT_ILP") && atoi(getenv("RPG_JIT_ILP")) == 2);
+  if (buf && buflen) {
+    const size_t n = std::min(buflen - 1, src.size());
+    memcpy(buf, src.data(), n);
+    buf[n] = '\0';
+  }
+  if (compile) {
+    std::vector<char> cubin;
+    std::string log;
+    if (rpg_jit::compile(src, 2, &cubin, &log) != 0)
+      return set_err(err, errlen, RPG_E_CUDA, "NVRTC: %s", log.substr(0, 1500).c_str());
+    if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
+  }
+  return (int64_t)src.size();
+}
+
+extern "C" int64_t rpg_emit_program_cuda_source(const rpg_program* prog, const rpg_profile* hw,
+                                                const rpg_options* opts, int32_t compile,
+                                                char* buf, size_t buflen, int64_t* cubin_bytes,
+                                                char* err, size_t errlen) {
+  if (!prog || !hw || !opts)
+    return set_err(err, errlen, RPG_E_INVALID, "rpg_emit_program_cuda_source: null argument");
+  Params P;
+  ModelTables tab;
+  int rc = prepare_program(prog, hw, opts, P, tab, err, errlen);
+  if (rc) return rc;
+  const std::string src = rpg_jit::generate_program_source(*prog, P);
   if (buf && buflen) {
     const size_t n = std::min(buflen - 1, src.size());
     memcpy(buf, src.data(), n);

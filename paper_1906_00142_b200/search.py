@@ -18,6 +18,7 @@ import numpy as np
 
 from . import abi as A
 from . import formats as F
+from . import program as P
 
 
 class NoFeasibleConfig(RuntimeError):
@@ -80,34 +81,69 @@ def _raise(code: int, err) -> None:
         raise F.PipelineError(msg)
     if code == A.RPG_E_NO_FEASIBLE:
         raise NoFeasibleConfig(msg)
+    if code == A.RPG_E_EVAL:
+        raise P.EvalError(msg)
     raise A.RpgError(code, msg)
 
 
 class Plan:
-    """A metric spec + profile + configuration space resident on one GPU."""
+    """A rational program plus profile and configuration space resident on
+    one GPU.  ``source`` is a metric spec (the ``--models`` path: the
+    emitted MWP-CWP program, pipeline.hpp:251-255) or a bare program
+    (``program.Program`` / ``.rp`` text, the ``--rp`` path)."""
 
-    def __init__(self, spec: F.MetricSpec, hw: F.DeviceProfile,
+    def __init__(self, source, hw: F.DeviceProfile,
                  space: Sequence[Tuple[int, int, int]],
-                 opts: Optional[SearchOptions] = None):
+                 opts: Optional[SearchOptions] = None, step_limit: int = 1_000_000):
         self.lib = A.load_library()
         self.opts = opts or SearchOptions()
-        self.spec = spec
         self.hw = hw
-        self.packed = A.PackedModel(spec)
         self.hw_struct = A.profile_struct(hw)
         self.space = A.config_array(list(space))
         self.n_space = len(self.space)
-        self.d = F.data_param_count(spec)
         self._handle = C.c_void_p()
+        self.lowered: Optional[P.LoweredProgram] = None
         err = C.create_string_buffer(512)
         opts_s = self.opts.struct()
-        rc = self.lib.rpg_plan_create(
-            C.byref(self.packed.struct), C.byref(self.hw_struct),
-            A.ptr(self.space, A.rpg_config) if self.n_space else None,
-            self.n_space, C.byref(opts_s), self.opts.device,
-            C.byref(self._handle), err, len(err))
+        space_p = A.ptr(self.space, A.rpg_config) if self.n_space else None
+        if isinstance(source, (str, P.Program)):
+            prog = P.parse(source) if isinstance(source, str) else source
+            if self.n_space == 0:
+                raise ValueError("search_optimal: configuration space is empty")
+            self.spec = None
+            self.lowered = P.LoweredProgram(prog, hw, step_limit)
+            self.d = self.lowered.max_data_index() + 1
+            rc = self.lib.rpg_program_plan_create(
+                C.cast(C.pointer(self.lowered.struct), C.c_void_p), C.byref(self.hw_struct),
+                space_p, self.n_space, C.byref(opts_s), self.opts.device,
+                C.byref(self._handle), err, len(err))
+        else:
+            self.spec = source
+            self.packed = A.PackedModel(source)
+            self.d = F.data_param_count(source)
+            rc = self.lib.rpg_plan_create(
+                C.byref(self.packed.struct), C.byref(self.hw_struct), space_p,
+                self.n_space, C.byref(opts_s), self.opts.device,
+                C.byref(self._handle), err, len(err))
         if rc != A.RPG_OK:
             _raise(rc, err)
+
+    def _check(self, rc: int, err, n_data: Optional[int] = None) -> None:
+        if rc == A.RPG_OK:
+            return
+        if self.lowered is not None:
+            if rc == A.RPG_E_EVAL:
+                self.lowered.raise_eval_error(err.value.decode(errors="replace"))
+            if rc == A.RPG_E_PIPELINE and n_data is not None:
+                self.lowered.check_binding(n_data)
+        _raise(rc, err)
+
+    def poll_error(self, stream_ptr: int = 0) -> None:
+        """Raises the first evaluation error of earlier _device calls on a
+        bare-program plan (rpg_plan_poll_error)."""
+        err = C.create_string_buffer(512)
+        self._check(self.lib.rpg_plan_poll_error(self._handle, C.c_void_p(stream_ptr),
+                                                 err, len(err)), err)
 
     def close(self) -> None:
         if self._handle:
@@ -139,10 +175,11 @@ class Plan:
         n, d = a.shape
         out = np.zeros(n, dtype=A.WINNER_DTYPE)
         err = C.create_string_buffer(512)
+        if self.lowered is not None:
+            self.lowered.check_binding(d)
         rc = self.lib.rpg_search_batch(self._handle, A.ptr(a, C.c_int64), n, d,
                                        out.ctypes.data_as(C.c_void_p), err, len(err))
-        if rc != A.RPG_OK:
-            _raise(rc, err)
+        self._check(rc, err, d)
         return out
 
     def search_batch_device(self, d_data_ptr: int, n: int, d: int,
@@ -152,8 +189,7 @@ class Plan:
         rc = self.lib.rpg_search_batch_device(self._handle, C.c_void_p(d_data_ptr), n, d,
                                               C.c_void_p(d_out_ptr), C.c_void_p(stream_ptr),
                                               err, len(err))
-        if rc != A.RPG_OK:
-            _raise(rc, err)
+        self._check(rc, err, d)
 
     def evaluate(self, data):
         """Per-point table: (Ec, case tag, occupancy warps), tuple-major."""
@@ -163,11 +199,12 @@ class Plan:
         tag = np.zeros((n, self.n_space), dtype=np.uint8)
         wocc = np.zeros((n, self.n_space), dtype=np.int32)
         err = C.create_string_buffer(512)
+        if self.lowered is not None:
+            self.lowered.check_binding(d)
         rc = self.lib.rpg_evaluate(self._handle, A.ptr(a, C.c_int64), n, d,
                                    ec.ctypes.data_as(C.c_void_p), tag.ctypes.data_as(C.c_void_p),
                                    wocc.ctypes.data_as(C.c_void_p), err, len(err))
-        if rc != A.RPG_OK:
-            _raise(rc, err)
+        self._check(rc, err, d)
         return ec, tag, wocc
 
     def evaluate_device(self, d_data_ptr: int, n: int, d: int, d_ec: int,
@@ -177,8 +214,7 @@ class Plan:
                                           C.c_void_p(d_ec), C.c_void_p(d_tag),
                                           C.c_void_p(d_wocc), C.c_void_p(stream_ptr),
                                           err, len(err))
-        if rc != A.RPG_OK:
-            _raise(rc, err)
+        self._check(rc, err, d)
 
     def config(self, idx: int) -> Tuple[int, int, int]:
         r = self.space[idx]
@@ -213,23 +249,26 @@ def ranking_from_table(space: np.ndarray, ec: np.ndarray, tag: np.ndarray,
     return res
 
 
-def search_optimal(spec: F.MetricSpec, data_params: Sequence[int],
+def search_optimal(source, data_params: Sequence[int],
                    hw: F.DeviceProfile, space: Sequence[Tuple[int, int, int]],
-                   opts: Optional[SearchOptions] = None) -> SearchResult:
-    """pipe::search_optimal for the metric-spec path (one data tuple)."""
+                   opts: Optional[SearchOptions] = None,
+                   step_limit: int = 1_000_000) -> SearchResult:
+    """pipe::search_optimal (pipeline.hpp:575-680) for one data tuple;
+    ``source`` is a metric spec or a bare program (``program.Program`` or
+    ``.rp`` text)."""
     if len(space) == 0:
         raise ValueError("search_optimal: configuration space is empty")
     opts = opts or SearchOptions()
-    with Plan(spec, hw, space, opts) as plan:
+    with Plan(source, hw, space, opts, step_limit=step_limit) as plan:
         data = np.asarray([list(data_params)], dtype=np.int64).reshape(1, len(data_params))
         ec, tag, wocc = plan.evaluate(data)
         return ranking_from_table(plan.space, ec[0], tag[0], wocc[0], hw.W_max,
                                   opts.tie_rel_tol)
 
 
-def search_optimal_batch(spec: F.MetricSpec, data: Sequence[Sequence[int]],
+def search_optimal_batch(source, data: Sequence[Sequence[int]],
                          hw: F.DeviceProfile, space: Sequence[Tuple[int, int, int]],
                          opts: Optional[SearchOptions] = None) -> np.ndarray:
     """Batched search: one winner record per data tuple."""
-    with Plan(spec, hw, space, opts) as plan:
+    with Plan(source, hw, space, opts) as plan:
         return plan.search_batch(data)
