@@ -295,6 +295,42 @@ int64_t rpg_emit_program_cuda_source(const rpg_program* prog, const rpg_profile*
  * failing tuple/configuration), or RPG_OK.  No-op for metric-spec plans. */
 int rpg_plan_poll_error(rpg_plan* plan, void* stream, char* err, size_t errlen);
 
+/* search_optimal over a per-tuple subset of the plan's configuration space
+ * (sanity_report searches each data tuple over its own sampled
+ * configurations, pipeline.hpp:816-824): tuple t searches the space indices
+ * list[offsets[t] .. offsets[t+1]) (distinct, any order; offsets[0] = 0).
+ * Ranking, ties and counts are those of search_optimal over that subset. */
+int rpg_search_batch_subsets(rpg_plan* plan, const int64_t* data, int64_t n_tuples,
+                             int32_t d, const int64_t* offsets, const int32_t* list,
+                             rpg_winner* out, char* err, size_t errlen);
+int rpg_search_batch_subsets_device(rpg_plan* plan, const int64_t* d_data,
+                                    int64_t n_tuples, int32_t d, const int64_t* d_offsets,
+                                    const int32_t* d_list, rpg_winner* d_out, void* stream,
+                                    char* err, size_t errlen);
+
+/* perf::mwpcwp_cycles (perfmodel.hpp:298-395) over n rows of given metric
+ * values (n x RPG_N_METRICS, RPG_METRIC_* order; mem = uncoal + coal as
+ * metrics_from_sample forms it, pipeline.hpp:733-752) and configurations:
+ * the direct model, IEEE arithmetic in the reference's order.  Per row:
+ * total cycles, resident blocks / warps, case tag, and status 0 = ok,
+ * 1 = ZeroOccupancy, 2 = ModelError (negative metric), 3 = ModelError
+ * (inconsistent mem).  Output pointers other than status_out may be NULL. */
+int rpg_mwpcwp_cycles_batch(const rpg_profile* hw, const double* metrics,
+                            const rpg_config* configs, int64_t n, int32_t rep_mode,
+                            int32_t device, double* total_out, int32_t* b_out,
+                            int32_t* w_out, uint8_t* tag_out, int32_t* status_out,
+                            char* err, size_t errlen);
+
+/* poly::eval_ratfunc (polyfit.hpp:96-130) at m points X (m x n_vars): out =
+ * p/q, status 1 where DenominatorNearZero (|q| < 1e-12 max(1, |p|)). */
+int rpg_eval_ratfunc_batch(const rpg_poly* num, const rpg_poly* den, int32_t n_vars,
+                           const double* X, int64_t m, int32_t device, double* out,
+                           int32_t* status_out, char* err, size_t errlen);
+
+/* n draws of rng::uniform_real(lo, hi) (rng.hpp:14-21) from
+ * std::mt19937_64(seed), in order (host). */
+int rpg_uniform_stream(uint64_t seed, int64_t n, double lo, double hi, double* out);
+
 /* One-shot convenience for FFI callers. */
 int rpg_search(const rpg_model* model, const rpg_profile* hw,
                const rpg_config* space, int64_t n_space,

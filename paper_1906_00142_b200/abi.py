@@ -214,6 +214,21 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                                      C.POINTER(rpg_options), C.c_int32,
                                                      C.c_char_p, C.c_size_t,
                                                      C.POINTER(C.c_int64)) + errbuf),
+        "rpg_search_batch_subsets": (C.c_int, (C.c_void_p, C.POINTER(C.c_int64), C.c_int64,
+                                               C.c_int32, C.POINTER(C.c_int64),
+                                               C.POINTER(C.c_int32), C.c_void_p) + errbuf),
+        "rpg_search_batch_subsets_device": (C.c_int, (C.c_void_p, C.c_void_p, C.c_int64,
+                                                      C.c_int32, C.c_void_p, C.c_void_p,
+                                                      C.c_void_p, C.c_void_p) + errbuf),
+        "rpg_mwpcwp_cycles_batch": (C.c_int, (C.POINTER(rpg_profile), C.POINTER(C.c_double),
+                                              C.POINTER(rpg_config), C.c_int64, C.c_int32,
+                                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_void_p) + errbuf),
+        "rpg_eval_ratfunc_batch": (C.c_int, (C.POINTER(rpg_poly), C.POINTER(rpg_poly), C.c_int32,
+                                             C.POINTER(C.c_double), C.c_int64, C.c_int32,
+                                             C.POINTER(C.c_double), C.POINTER(C.c_int32)) + errbuf),
+        "rpg_uniform_stream": (C.c_int, (C.c_uint64, C.c_int64, C.c_double, C.c_double,
+                                         C.POINTER(C.c_double))),
         "rpg_search": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
                                  C.POINTER(rpg_config), C.c_int64,
                                  C.POINTER(rpg_options), C.POINTER(C.c_int64),
@@ -232,7 +247,9 @@ EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_search_batch_device", "rpg_evaluate",
                     "rpg_evaluate_device", "rpg_search", "rpg_emit_cuda_source",
                     "rpg_fit_rational", "rpg_program_plan_create",
-                    "rpg_plan_poll_error", "rpg_emit_program_cuda_source")
+                    "rpg_plan_poll_error", "rpg_emit_program_cuda_source",
+                    "rpg_search_batch_subsets", "rpg_search_batch_subsets_device",
+                    "rpg_mwpcwp_cycles_batch", "rpg_eval_ratfunc_batch", "rpg_uniform_stream")
 
 
 class RpgError(RuntimeError):

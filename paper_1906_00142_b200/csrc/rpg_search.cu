@@ -628,10 +628,13 @@ int check_arity(const rpg_plan* plan, int32_t d, char* err, size_t errlen) {
 }
 
 int launch_search(rpg_plan* plan, const int64_t* d_data, int64_t n, int32_t d,
-                  rpg_winner* d_out, cudaStream_t s, char* err, size_t errlen) {
+                  rpg_winner* d_out, cudaStream_t s, char* err, size_t errlen,
+                  const int64_t* d_sub_off = nullptr, const int32_t* d_sub_list = nullptr) {
   if (n <= 0) return RPG_OK;
   Params P = plan->P;
   P.d = d;
+  P.sub_off = d_sub_off;
+  P.sub_list = d_sub_list;
   const int grid = (int)std::min<int64_t>(n, plan->grid_search);
   void* args[] = {&P, &d_data, &n, &d_out};
   CUDA_TRY(cudaLaunchKernel(search_fn(plan), dim3(grid), dim3(kThreads), args, plan->smem, s));
@@ -729,6 +732,82 @@ int rpg_evaluate(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int32_t 
   return plan->is_program ? take_program_error(plan, err, errlen) : RPG_OK;
 }
 
+// Host-side check of a CSR subset description (offsets[0] = 0,
+// non-decreasing, entries in range and distinct per tuple).
+static int check_subsets(const rpg_plan* plan, int64_t n_tuples, const int64_t* off,
+                         const int32_t* list, char* err, size_t errlen) {
+  if (!off || (off[n_tuples] > 0 && !list))
+    return set_err(err, errlen, RPG_E_INVALID, "subsets: null offsets or list");
+  if (off[0] != 0) return set_err(err, errlen, RPG_E_INVALID, "subsets: offsets[0] must be 0");
+  std::vector<int64_t> seen((size_t)plan->P.n_space, -1);
+  for (int64_t t = 0; t < n_tuples; ++t) {
+    if (off[t + 1] < off[t])
+      return set_err(err, errlen, RPG_E_INVALID, "subsets: offsets must be non-decreasing");
+    if (off[t + 1] - off[t] > plan->P.n_space)
+      return set_err(err, errlen, RPG_E_INVALID, "subsets: tuple %lld lists more configurations "
+                     "than the space holds", (long long)t);
+    for (int64_t k = off[t]; k < off[t + 1]; ++k) {
+      const int32_t c = list[k];
+      if (c < 0 || c >= plan->P.n_space)
+        return set_err(err, errlen, RPG_E_INVALID, "subsets: configuration index %d out of range", c);
+      if (seen[(size_t)c] == t)
+        return set_err(err, errlen, RPG_E_INVALID, "subsets: configuration %d listed twice for "
+                       "tuple %lld", c, (long long)t);
+      seen[(size_t)c] = t;
+    }
+  }
+  return RPG_OK;
+}
+
+int rpg_search_batch_subsets_device(rpg_plan* plan, const int64_t* d_data, int64_t n_tuples,
+                                    int32_t d, const int64_t* d_offsets, const int32_t* d_list,
+                                    rpg_winner* d_out, void* stream, char* err, size_t errlen) {
+  if (!plan) return set_err(err, errlen, RPG_E_INVALID, "null plan");
+  int rc = check_arity(plan, d, err, errlen);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(plan->device));
+  return launch_search(plan, d_data, n_tuples, d, d_out, (cudaStream_t)stream, err, errlen,
+                       d_offsets, d_list);
+}
+
+int rpg_search_batch_subsets(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int32_t d,
+                             const int64_t* offsets, const int32_t* list, rpg_winner* out,
+                             char* err, size_t errlen) {
+  if (!plan) return set_err(err, errlen, RPG_E_INVALID, "null plan");
+  int rc = check_arity(plan, d, err, errlen);
+  if (rc) return rc;
+  if (n_tuples <= 0) return RPG_OK;
+  if ((rc = check_subsets(plan, n_tuples, offsets, list, err, errlen))) return rc;
+  std::lock_guard<std::mutex> lock(plan->mu);
+  CUDA_TRY(cudaSetDevice(plan->device));
+  const int64_t n_list = offsets[n_tuples];
+  const size_t in_bytes = sizeof(int64_t) * (size_t)n_tuples * (size_t)std::max(d, 1);
+  const size_t out_bytes = sizeof(rpg_winner) * (size_t)n_tuples;
+  const size_t off_bytes = sizeof(int64_t) * (size_t)(n_tuples + 1);
+  const size_t list_bytes = sizeof(int32_t) * (size_t)std::max<int64_t>(n_list, 1);
+  CUDA_TRY(ensure(&plan->d_data, &plan->d_data_cap, in_bytes));
+  CUDA_TRY(ensure(reinterpret_cast<char**>(&plan->d_out), &plan->d_out_cap,
+                  out_bytes + off_bytes + list_bytes + 16));
+  char* base = reinterpret_cast<char*>(plan->d_out);
+  int64_t* d_off = reinterpret_cast<int64_t*>(base + ((out_bytes + 7) & ~(size_t)7));
+  int32_t* d_list = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(d_off) + off_bytes);
+  if (d > 0)
+    CUDA_TRY(cudaMemcpyAsync(plan->d_data, data, sizeof(int64_t) * (size_t)n_tuples * d,
+                             cudaMemcpyHostToDevice, plan->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_off, offsets, off_bytes, cudaMemcpyHostToDevice, plan->stream));
+  if (n_list > 0)
+    CUDA_TRY(cudaMemcpyAsync(d_list, list, sizeof(int32_t) * (size_t)n_list,
+                             cudaMemcpyHostToDevice, plan->stream));
+  if (plan->is_program)
+    CUDA_TRY(cudaMemsetAsync(plan->d_err, 0xff, sizeof(unsigned long long), plan->stream));
+  rc = launch_search(plan, plan->d_data, n_tuples, d, (rpg_winner*)plan->d_out, plan->stream,
+                     err, errlen, d_off, d_list);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, plan->d_out, out_bytes, cudaMemcpyDeviceToHost, plan->stream));
+  CUDA_TRY(cudaStreamSynchronize(plan->stream));
+  return plan->is_program ? take_program_error(plan, err, errlen) : RPG_OK;
+}
+
 int rpg_search(const rpg_model* model, const rpg_profile* hw, const rpg_config* space,
                int64_t n_space, const rpg_options* opts, const int64_t* data, int64_t n_tuples,
                int32_t d, int32_t device, rpg_winner* out, char* err, size_t errlen) {
@@ -794,4 +873,219 @@ extern "C" int64_t rpg_emit_program_cuda_source(const rpg_program* prog, const r
     if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
   }
   return (int64_t)src.size();
+}
+
+// ---------------------------------------------------------------------------
+// perf::mwpcwp_cycles over a batch of (metrics, configuration) rows — the
+// "collected" side of sanity_report (pipeline.hpp:797-814) and any caller of
+// the direct model.  IEEE arithmetic in the reference's operation order.
+namespace {
+
+__global__ void direct_cycles_kernel(const Params P, const double* __restrict__ metrics,
+                                     const rpg_config* __restrict__ cfgs, int64_t n,
+                                     double* __restrict__ total, int32_t* __restrict__ b_out,
+                                     int32_t* __restrict__ w_out, uint8_t* __restrict__ tag_out,
+                                     int32_t* __restrict__ status) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* mv = metrics + i * RPG_N_METRICS;
+    Metrics m;
+    m.regs = mv[RPG_METRIC_REGS];
+    m.shared = mv[RPG_METRIC_SHARED];
+    m.comp = mv[RPG_METRIC_COMP];
+    m.uncoal = mv[RPG_METRIC_UNCOAL];
+    m.coal = mv[RPG_METRIC_COAL];
+    m.mem = __dadd_rn(m.uncoal, m.coal);  // metrics_from_sample (pipeline.hpp:746-747)
+    m.synch = mv[RPG_METRIC_SYNCH];
+    m.tb = mv[RPG_METRIC_TOTAL_BLOCKS];
+    int st = 0, tag = RPG_CASE_UNKNOWN;
+    int64_t b = 0, W = 0;
+    double ec = 0.0;
+    // perfmodel.hpp:302-310
+    const double chk = __dadd_rn(__dadd_rn(m.uncoal, m.coal), -m.mem);
+    if (fabs(chk) > __dmul_rn(1e-9, m.mem > 1.0 ? m.mem : 1.0)) st = 3;
+    else if (metrics_negative(m)) st = 2;
+    if (!st) {
+      const rpg_config c = cfgs[i];
+      const int64_t T = c.bx * c.by * c.bz;
+      b = active_blocks(P.hw, m.regs, m.shared, T, false);
+      W = b ? active_warps(P.hw, b, T) : 0;
+      if (b == 0 || W == 0) {
+        st = 1;
+      } else {
+        bool ok = true;
+        ec = mwpcwp_core<IeeeDiv>(P, m, b, W, false, &tag, ok);
+      }
+    }
+    if (total) total[i] = ec;
+    if (b_out) b_out[i] = (int32_t)b;
+    if (w_out) w_out[i] = (int32_t)W;
+    if (tag_out) tag_out[i] = (uint8_t)tag;
+    if (status) status[i] = st;
+  }
+}
+
+// poly::eval_ratfunc (polyfit.hpp:96-130) over m points: basis-order
+// products and sums, DenominatorNearZero flagged (status 1).
+__global__ void ratfunc_kernel(const double* __restrict__ num_c, const uint8_t* __restrict__ num_e,
+                               int32_t n_num, const double* __restrict__ den_c,
+                               const uint8_t* __restrict__ den_e, int32_t n_den, int32_t nv,
+                               const double* __restrict__ X, int64_t m,
+                               double* __restrict__ out, int32_t* __restrict__ status) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* x = X + i * nv;
+    auto poly = [&](const double* c, const uint8_t* e, int nt) {
+      double acc = 0.0;
+      for (int k = 0; k < nt; ++k) {
+        double mono = 1.0;
+        for (int v = 0; v < nv; ++v) {  // eval_monomial: per-variable power, then product
+          double pw = 1.0;
+          for (int j = 0; j < e[k * nv + v]; ++j) pw = __dmul_rn(pw, x[v]);
+          mono = __dmul_rn(mono, pw);
+        }
+        acc = __dadd_rn(acc, __dmul_rn(c[k], mono));
+      }
+      return acc;
+    };
+    const double p = poly(num_c, num_e, n_num);
+    const double q = poly(den_c, den_e, n_den);
+    const double mag = fabs(p);
+    if (fabs(q) < __dmul_rn(1e-12, mag > 1.0 ? mag : 1.0)) {
+      out[i] = 0.0;
+      status[i] = 1;
+    } else {
+      out[i] = __ddiv_rn(p, q);
+      status[i] = 0;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int rpg_mwpcwp_cycles_batch(const rpg_profile* hw, const double* metrics,
+                                       const rpg_config* configs, int64_t n, int32_t rep_mode,
+                                       int32_t device, double* total_out, int32_t* b_out,
+                                       int32_t* w_out, uint8_t* tag_out, int32_t* status_out,
+                                       char* err, size_t errlen) {
+  if (!hw || (n > 0 && (!metrics || !configs || !status_out)))
+    return set_err(err, errlen, RPG_E_INVALID, "rpg_mwpcwp_cycles_batch: null argument");
+  int rc = validate_profile(hw, err, errlen);
+  if (rc) return rc;
+  if (rep_mode != RPG_REP_REAL && rep_mode != RPG_REP_CEIL)
+    return set_err(err, errlen, RPG_E_INVALID, "rep_mode must be real or ceil");
+  if (n <= 0) return RPG_OK;
+  Params P{};
+  P.hw = *hw;
+  hoist_hardware(P);
+  P.rep_mode = rep_mode;
+  CUDA_TRY(cudaSetDevice(device));
+  cudaStream_t s;
+  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  char* buf = nullptr;
+  const size_t in_m = sizeof(double) * RPG_N_METRICS * (size_t)n;
+  const size_t in_c = sizeof(rpg_config) * (size_t)n;
+  const size_t o_t = sizeof(double) * (size_t)n, o_i = sizeof(int32_t) * (size_t)n;
+  const size_t total = in_m + in_c + o_t + 3 * o_i + (size_t)n + 64;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), total, s);
+  if (e == cudaSuccess) {
+    double* d_m = reinterpret_cast<double*>(buf);
+    rpg_config* d_c = reinterpret_cast<rpg_config*>(buf + in_m);
+    double* d_t = reinterpret_cast<double*>(buf + in_m + in_c);
+    int32_t* d_b = reinterpret_cast<int32_t*>(buf + in_m + in_c + o_t);
+    int32_t* d_w = d_b + n;
+    int32_t* d_s = d_w + n;
+    uint8_t* d_g = reinterpret_cast<uint8_t*>(d_s + n);
+    cudaMemcpyAsync(d_m, metrics, in_m, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_c, configs, in_c, cudaMemcpyHostToDevice, s);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+    direct_cycles_kernel<<<grid, 256, 0, s>>>(P, d_m, d_c, n, d_t, d_b, d_w, d_g, d_s);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      if (total_out) cudaMemcpyAsync(total_out, d_t, o_t, cudaMemcpyDeviceToHost, s);
+      if (b_out) cudaMemcpyAsync(b_out, d_b, o_i, cudaMemcpyDeviceToHost, s);
+      if (w_out) cudaMemcpyAsync(w_out, d_w, o_i, cudaMemcpyDeviceToHost, s);
+      if (tag_out) cudaMemcpyAsync(tag_out, d_g, (size_t)n, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(status_out, d_s, o_i, cudaMemcpyDeviceToHost, s);
+      e = cudaStreamSynchronize(s);
+    }
+    cudaFreeAsync(buf, s);
+  }
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess)
+    return set_err(err, errlen, RPG_E_CUDA, "rpg_mwpcwp_cycles_batch: %s", cudaGetErrorString(e));
+  return RPG_OK;
+}
+
+extern "C" int rpg_eval_ratfunc_batch(const rpg_poly* num, const rpg_poly* den, int32_t n_vars,
+                                      const double* X, int64_t m, int32_t device, double* out,
+                                      int32_t* status_out, char* err, size_t errlen) {
+  if (!num || !den || (m > 0 && (!X || !out || !status_out)))
+    return set_err(err, errlen, RPG_E_INVALID, "rpg_eval_ratfunc_batch: null argument");
+  if (n_vars < 1 || n_vars > RPG_MAX_VARS || num->n_terms < 0 || den->n_terms < 0)
+    return set_err(err, errlen, RPG_E_INVALID, "rpg_eval_ratfunc_batch: bad shape");
+  if (m <= 0) return RPG_OK;
+  CUDA_TRY(cudaSetDevice(device));
+  cudaStream_t s;
+  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const size_t tn = (size_t)std::max(num->n_terms, 1), td = (size_t)std::max(den->n_terms, 1);
+  const size_t bx = sizeof(double) * (size_t)m * n_vars;
+  const size_t total = bx + sizeof(double) * (size_t)m + sizeof(int32_t) * (size_t)m +
+                       sizeof(double) * (tn + td) + (tn + td) * n_vars + 64;
+  char* buf = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), total, s);
+  if (e == cudaSuccess) {
+    double* d_x = reinterpret_cast<double*>(buf);
+    double* d_o = reinterpret_cast<double*>(buf + bx);
+    double* d_nc = d_o + m;
+    double* d_dc = d_nc + tn;
+    int32_t* d_s = reinterpret_cast<int32_t*>(d_dc + td);
+    uint8_t* d_ne = reinterpret_cast<uint8_t*>(d_s + m);
+    uint8_t* d_de = d_ne + tn * n_vars;
+    cudaMemcpyAsync(d_x, X, bx, cudaMemcpyHostToDevice, s);
+    if (num->n_terms) {
+      cudaMemcpyAsync(d_nc, num->coef, sizeof(double) * num->n_terms, cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(d_ne, num->exps, (size_t)num->n_terms * n_vars, cudaMemcpyHostToDevice, s);
+    }
+    if (den->n_terms) {
+      cudaMemcpyAsync(d_dc, den->coef, sizeof(double) * den->n_terms, cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(d_de, den->exps, (size_t)den->n_terms * n_vars, cudaMemcpyHostToDevice, s);
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)sms * 8);
+    ratfunc_kernel<<<grid, 256, 0, s>>>(d_nc, d_ne, num->n_terms, d_dc, d_de, den->n_terms,
+                                        n_vars, d_x, m, d_o, d_s);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      cudaMemcpyAsync(out, d_o, sizeof(double) * (size_t)m, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(status_out, d_s, sizeof(int32_t) * (size_t)m, cudaMemcpyDeviceToHost, s);
+      e = cudaStreamSynchronize(s);
+    }
+    cudaFreeAsync(buf, s);
+  }
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess)
+    return set_err(err, errlen, RPG_E_CUDA, "rpg_eval_ratfunc_batch: %s", cudaGetErrorString(e));
+  return RPG_OK;
+}
+
+// rng::uniform_real draws (rng.hpp:14-21) from std::mt19937_64(seed): the
+// noise stream of data::synthesize (datakit.hpp:199-203), which is
+// sequential by construction (one draw per kept point and metric).
+#include <random>
+extern "C" int rpg_uniform_stream(uint64_t seed, int64_t n, double lo, double hi, double* out) {
+  if (n < 0 || (n > 0 && !out)) return RPG_E_INVALID;
+  std::mt19937_64 g(seed);
+  const double span = hi - lo;
+  for (int64_t i = 0; i < n; ++i) {
+    const double c = static_cast<double>(g() >> 11) * 0x1.0p-53;
+    const double t = span * c;  // -ffp-contract=off: no fused multiply-add
+    out[i] = lo + t;
+  }
+  return RPG_OK;
 }

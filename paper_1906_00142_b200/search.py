@@ -182,6 +182,26 @@ class Plan:
         self._check(rc, err, d)
         return out
 
+    def search_batch_subsets(self, data, offsets, cfg_list) -> np.ndarray:
+        """Winners when tuple t searches only the space indices
+        cfg_list[offsets[t]:offsets[t+1]] (rpg_search_batch_subsets)."""
+        a = self._data(data)
+        n, d = a.shape
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        lst = np.ascontiguousarray(cfg_list, dtype=np.int32)
+        if len(off) != n + 1:
+            raise ValueError("search_batch_subsets: need n_tuples + 1 offsets")
+        out = np.zeros(n, dtype=A.WINNER_DTYPE)
+        err = C.create_string_buffer(512)
+        if self.lowered is not None:
+            self.lowered.check_binding(d)
+        rc = self.lib.rpg_search_batch_subsets(
+            self._handle, A.ptr(a, C.c_int64), n, d, A.ptr(off, C.c_int64),
+            A.ptr(lst, C.c_int32) if len(lst) else None, out.ctypes.data_as(C.c_void_p),
+            err, len(err))
+        self._check(rc, err, d)
+        return out
+
     def search_batch_device(self, d_data_ptr: int, n: int, d: int,
                             d_out_ptr: int, stream_ptr: int) -> None:
         """Device-resident variant (raw device pointers, cudaStream_t)."""
