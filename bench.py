@@ -12,6 +12,12 @@ per GPU.  Multi-GPU: rank r sweeps the next 65,473 N values (weak scaling
 along the data-parameter axis) and the per-N winner records are all-gathered
 over NCCL inside the timed region.
 
+`--workload c3` sweeps the full 27-kernel PolyBench-GPU suite (configs[2]:
+N = 64..65,536 split over the GPUs, strong scaling) and `--workload c5` the
+5-variable stress model over a 182 x 182 (N, M) grid x 30,343 3-D blocks
+(configs[4], 1.005e9 evaluations, strong scaling); they are extra lines, the
+default stays C2.
+
 Prints one JSON line (rank 0).  `--impl reference` times the CPU
 restatement of the reference path (oracle O1, all host cores) on a bounded
 sample of the same workload instead.
@@ -38,14 +44,63 @@ N0 = 64
 METRIC = "MWP-CWP config evaluations/sec"
 UNIT = "evals/s"
 
+# Full PolyBench-GPU suite, paper kernel-ID order (config C3).
+SUITE = ("2dconv", "fdtd2d_step1", "fdtd2d_step2", "fdtd2d_step3", "2mm1", "3mm1", "bicg1", "bicg2",
+         "gemm", "3dconv", "atax1", "atax2", "gesummv", "syrk", "mvt1", "mvt2", "syr2k",
+         "corr", "corr_mean", "corr_reduce", "corr_std", "covar", "covar_mean", "covar_reduce",
+         "gramschmidt1", "gramschmidt2", "gramschmidt3")
+C5_GRID = 182               # (N, M) grid 182 x 182 = 33,124 tuples
+
+
+class Workload:
+    """One BASELINE.json config: models, config space and the data tuples
+    each rank sweeps.  c2 = configs[1] (the bench default, weak scaling along
+    N), c3 = configs[2] (all 27 suite kernels, fixed N range split over the
+    ranks), c5 = configs[4] (5-variable model, 3-D blocks, (N, M) grid split
+    over the ranks)."""
+
+    def __init__(self, name: str):
+        from paper_1906_00142_b200 import formats as F
+        self.name = name
+        self.hw = F.load_profile(os.path.join(ROOT, "data", "b200.profile"))
+        if name == "c5":
+            self.kernels = ("stencil3d_nm",)
+            path = os.path.join(ROOT, "data", "stress", "{}.models.json")
+            self.space = F.integer_configs(1024, dims=3)
+            self.scaling = "strong"
+            self.describe = ("C5 stress: 5-variable (D1,D2,bx,by,bz) 3-D stencil rational program (synthetic "
+                             "fitted form, default bounds 243+32 terms/metric), (N,M) grid 182x182 over "
+                             "[64,65536]^2 x 30343 integer (bx,by,bz), B200 profile")
+        else:
+            self.kernels = KERNELS if name == "c2" else SUITE
+            path = os.path.join(ROOT, "data", "polybench", "{}.models.json")
+            self.space = F.integer_configs(1024, dims=2)
+            self.scaling = "weak" if name == "c2" else "strong"
+            self.describe = ("C2: 2DCONV+GEMM+ATAX rational programs (synthetic fitted-form models, default "
+                             "bounds), dense N sweep, 7262 integer (bx,by) configs, B200 profile" if name == "c2" else
+                             "C3: full PolyBench-GPU suite, 27 kernels (synthetic fitted-form models, default "
+                             "bounds), N = 64..65536 every integer split over the GPUs, 7262 integer (bx,by)")
+        self.specs = {k: F.models_to_metric_spec(F.read_models(path.format(k))) for k in self.kernels}
+
+    def all_tuples(self) -> np.ndarray:
+        if self.name == "c5":
+            v = np.unique(np.linspace(N0, 65536, C5_GRID).round().astype(np.int64))
+            nn, mm = np.meshgrid(v, v, indexing="ij")
+            return np.stack([nn.ravel(), mm.ravel()], axis=1)
+        return np.arange(N0, N0 + N_PER_RANK, dtype=np.int64).reshape(-1, 1)
+
+    def tuples(self, rank: int, world: int) -> np.ndarray:
+        if self.scaling == "weak":
+            lo = N0 + rank * N_PER_RANK
+            return np.arange(lo, lo + N_PER_RANK, dtype=np.int64).reshape(-1, 1)
+        t = self.all_tuples()
+        per = -(-len(t) // world)   # contiguous blocks, as pipeline.hpp:602 partitions
+        return t[rank * per: (rank + 1) * per]
+
 
 def load_workload():
-    from paper_1906_00142_b200 import formats as F
-    hw = F.load_profile(os.path.join(ROOT, "data", "b200.profile"))
-    specs = {k: F.models_to_metric_spec(F.read_models(os.path.join(ROOT, "data", "polybench", f"{k}.models.json")))
-             for k in KERNELS}
-    space = F.integer_configs(1024, dims=2)
-    return hw, specs, space
+    w = Workload("c2")
+    return w.hw, w.specs, w.space
 
 
 def official_flops(spec) -> int:
@@ -135,35 +190,35 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU arms (oracle O1 = the CPU restatement of the reference path)
 
-def cpu_rate(seconds_target: float, threads: int, rng_seed: int = 0):
-    """Times O1's batched search on a bounded sample of the C2 workload."""
+def cpu_rate(wl: Workload, seconds_target: float, threads: int):
+    """Sizes a bounded sample of the workload for O1's batched search
+    (~seconds_target of CPU work): an evenly spread subset of the tuples."""
     from oracle import o1
     from paper_1906_00142_b200 import abi as A
-    hw, specs, space = load_workload()
-    sp = A.config_array(space)
-    hws = A.profile_struct(hw)
+    sp = A.config_array(wl.space)
+    hws = A.profile_struct(wl.hw)
     opts = A.options_struct()
-    packed = {k: A.PackedModel(specs[k], drop_zero_terms=False) for k in KERNELS}
-    # probe
+    packed = {k: A.PackedModel(wl.specs[k], drop_zero_terms=False) for k in wl.kernels}
+    allt = wl.all_tuples()
     probe = max(threads, 8)
-    ns = np.linspace(N0, N0 + N_PER_RANK - 1, probe).astype(np.int64).reshape(-1, 1)
+    pick = lambda n: np.ascontiguousarray(allt[np.linspace(0, len(allt) - 1, n).round().astype(np.int64)])
+    ns = pick(probe)
     t = time.perf_counter()
-    for k in KERNELS:
+    for k in wl.kernels:
         o1.search_batch(packed[k], hws, opts, sp, ns, threads)
     dt = time.perf_counter() - t
-    per_tuple = dt / (probe * len(KERNELS))
-    n = max(threads, int(seconds_target / per_tuple / len(KERNELS)))
-    ns = np.linspace(N0, N0 + N_PER_RANK - 1, n).astype(np.int64).reshape(-1, 1)
-    return packed, hws, opts, sp, ns
+    per_tuple = dt / (probe * len(wl.kernels))
+    n = min(len(allt), max(threads, int(seconds_target / per_tuple / len(wl.kernels))))
+    return packed, hws, opts, sp, pick(n)
 
 
 def run_cpu_sample(packed, hws, opts, sp, ns, threads):
     from oracle import o1
     t = time.perf_counter()
-    for k in KERNELS:
+    for k in packed:
         o1.search_batch(packed[k], hws, opts, sp, ns, threads)
     dt = time.perf_counter() - t
-    evals = len(KERNELS) * len(ns) * len(sp)
+    evals = len(packed) * len(ns) * len(sp)
     return evals / dt, dt, evals
 
 
@@ -179,26 +234,25 @@ def reference_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
+    wl = Workload(args.workload)
     threads = host_threads()
-    per_step_s = 4.0
-    packed, hws, opts, sp, ns = cpu_rate(per_step_s, threads)
+    packed, hws, opts, sp, ns = cpu_rate(wl, args.cpu_seconds / 2.5, threads)
     for _ in range(args.warmup):
         run_cpu_sample(packed, hws, opts, sp, ns[: max(threads, len(ns) // 4)], threads)
-    rates, times = [], []
+    times = []
     for _ in range(args.steps):
-        r, dt, evals = run_cpu_sample(packed, hws, opts, sp, ns, threads)
-        rates.append(r)
+        _, dt, _ = run_cpu_sample(packed, hws, opts, sp, ns, threads)
         times.append(dt)
-    value = len(KERNELS) * len(ns) * len(sp) * args.steps / sum(times)
-    sample = (f"{len(ns)} N values spread over [{N0}, {N0 + N_PER_RANK - 1}] x {len(sp)} configs "
-              f"x {len(KERNELS)} kernels per step (O1 batched search)")
+    value = len(packed) * len(ns) * len(sp) * args.steps / sum(times)
+    sample = (f"{len(ns)} data tuples spread evenly over the workload's tuples x {len(sp)} configs "
+              f"x {len(packed)} kernels per step (O1 batched search, {threads} threads)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": "C2 sample: 2DCONV+GEMM+ATAX fitted-form models x dense N sweep x 7262 (bx,by)",
+        "config": {"workload": wl.describe + " (bounded CPU sample)",
                    "oracle": "O1 (oracle/o1.c): FP64 CPU restatement of the reference path; the reference "
                              "itself (Eigen/Boost) cannot be built in this image"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
@@ -231,26 +285,32 @@ def gpu_arm(args):
     dev = torch.device("cuda", local)
     cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")  # collective buffers
 
-    hw, specs, space = load_workload()
+    wl = Workload(args.workload)
+    hw, specs, space = wl.hw, wl.specs, wl.space
     opts = S.SearchOptions(arith=args.arith, kernel=args.kernel, device=local)
-    plans = {k: S.Plan(specs[k], hw, space, opts) for k in KERNELS}
-    n = N_PER_RANK
-    lo = N0 + rank * n
-    data_host = np.arange(lo, lo + n, dtype=np.int64).reshape(n, 1)
+    plans = {k: S.Plan(specs[k], hw, space, opts) for k in wl.kernels}
+    data_host = wl.tuples(rank, world)
+    n_real = len(data_host)
+    if wl.scaling == "strong":   # equal-sized blocks for the all-gather; padding is not counted
+        per = -(-len(wl.all_tuples()) // world)
+        if n_real < per:
+            data_host = np.concatenate([data_host, np.repeat(data_host[-1:], per - n_real, axis=0)])
+    data_host = np.ascontiguousarray(data_host)
+    n, d = data_host.shape
     data_dev = torch.from_numpy(data_host).to(dev)
-    out_dev = {k: torch.empty(n * A.WINNER_DTYPE.itemsize, dtype=torch.uint8, device=dev) for k in KERNELS}
+    out_dev = {k: torch.empty(n * A.WINNER_DTYPE.itemsize, dtype=torch.uint8, device=dev) for k in wl.kernels}
     gathered = {k: torch.empty(world * n * A.WINNER_DTYPE.itemsize, dtype=torch.uint8, device=cdev)
-                for k in KERNELS} if world > 1 else None
+                for k in wl.kernels} if world > 1 else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
-    launches_per_step = len(KERNELS)
+    launches_per_step = len(wl.kernels)
 
     def step():
-        for k in KERNELS:
-            plans[k].search_batch_device(data_dev.data_ptr(), n, 1, out_dev[k].data_ptr(), sptr)
+        for k in wl.kernels:
+            plans[k].search_batch_device(data_dev.data_ptr(), n, d, out_dev[k].data_ptr(), sptr)
         if world > 1:
-            for k in KERNELS:
+            for k in wl.kernels:
                 dist.all_gather_into_tensor(gathered[k], out_dev[k].to(cdev))
 
     for _ in range(max(args.warmup, 3)):
@@ -279,8 +339,10 @@ def gpu_arm(args):
     if world > 1:
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     total_ms = float(total_ms.item())
-    evals_per_rank_step = len(KERNELS) * n * len(space)
-    value = world * evals_per_rank_step * args.steps / (total_ms / 1e3)
+    evals_per_rank_step = len(wl.kernels) * n * len(space)
+    # whole-job evaluations per step (padding of strong-scaling blocks not counted)
+    evals_job_step = len(wl.kernels) * len(space) * (world * n if wl.scaling == "weak" else len(wl.all_tuples()))
+    value = evals_job_step * args.steps / (total_ms / 1e3)
 
     # Kernel-only timing of the dominant kernel (the fused search kernel) on
     # the launching stream, for the roofline.
@@ -289,13 +351,13 @@ def gpu_arm(args):
         flush.fill_(1.0)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record(stream)
-        for k in KERNELS:
-            plans[k].search_batch_device(data_dev.data_ptr(), n, 1, out_dev[k].data_ptr(), sptr)
+        for k in wl.kernels:
+            plans[k].search_batch_device(data_dev.data_ptr(), n, d, out_dev[k].data_ptr(), sptr)
         ev[1].record(stream)
         ev[1].synchronize()
-        kt.append(ev[0].elapsed_time(ev[1]) / len(KERNELS))
+        kt.append(ev[0].elapsed_time(ev[1]) / len(wl.kernels))
     kernel_ms = statistics.median(kt)
-    flops_per_launch = statistics.mean(official_flops(specs[k]) for k in KERNELS) * n * len(space)
+    flops_per_launch = statistics.mean(official_flops(specs[k]) for k in wl.kernels) * n * len(space)
     achieved_tf = flops_per_launch / (kernel_ms / 1e3) / 1e12
     peak_tf, peak_src = fp64_peak_tflops()
     traffic = None
@@ -307,53 +369,54 @@ def gpu_arm(args):
     # ---- end-to-end through the public C-ABI host API (pinned host buffers)
     pinned = torch.from_numpy(data_host).pin_memory()
     pinned_np = pinned.numpy()
-    e2e_out = {k: np.zeros(n, dtype=A.WINNER_DTYPE) for k in KERNELS}
-    for k in KERNELS:  # warm the host-API staging buffers
+    e2e_out = {k: np.zeros(n, dtype=A.WINNER_DTYPE) for k in wl.kernels}
+    for k in wl.kernels:  # warm the host-API staging buffers
         plans[k].search_batch(pinned_np)
     if world > 1:
         dist.barrier()
     e2e_times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        for k in KERNELS:
+        for k in wl.kernels:
             e2e_out[k] = plans[k].search_batch(pinned_np)
         e2e_times.append(time.perf_counter() - t0)
     e2e_total = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(e2e_total, op=dist.ReduceOp.MAX)
-    e2e_value = world * evals_per_rank_step * args.steps / float(e2e_total.item())
-    h2d = len(KERNELS) * data_host.nbytes
-    d2h = len(KERNELS) * n * A.WINNER_DTYPE.itemsize
+    e2e_value = evals_job_step * args.steps / float(e2e_total.item())
+    h2d = len(wl.kernels) * data_host.nbytes
+    d2h = len(wl.kernels) * n * A.WINNER_DTYPE.itemsize
 
     # ---- agreement spot check against the device-API winners
-    chk = {k: out_dev[k].cpu().numpy().view(A.WINNER_DTYPE) for k in KERNELS}
-    agree = all(np.array_equal(chk[k], e2e_out[k]) for k in KERNELS)
+    chk = {k: out_dev[k].cpu().numpy().view(A.WINNER_DTYPE) for k in wl.kernels}
+    agree = all(np.array_equal(chk[k], e2e_out[k]) for k in wl.kernels)
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = host_threads()
-        packed, hws, o, sp, ns = cpu_rate(args.cpu_seconds, threads)
+        packed, hws, o, sp, ns = cpu_rate(wl, args.cpu_seconds, threads)
         rate, dt, evals = run_cpu_sample(packed, hws, o, sp, ns, threads)
         cpu_baseline = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                        "sample": f"O1 batched search, {len(ns)} N values x {len(sp)} configs x "
-                                  f"{len(KERNELS)} kernels ({evals:.3g} evals, {dt:.1f} s)"}
+                        "sample": f"O1 batched search, {len(ns)} data tuples x {len(sp)} configs x "
+                                  f"{len(wl.kernels)} kernels ({evals:.3g} evals, {dt:.1f} s)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2: 2DCONV+GEMM+ATAX rational programs (synthetic fitted-form models, "
-                                   "default bounds), dense N sweep, 7262 integer (bx,by) configs, B200 profile",
-                       "n_per_gpu": n, "n_range_rank0": [lo, lo + n - 1], "configs": len(space),
-                       "kernels": list(KERNELS), "evals_per_gpu_step": evals_per_rank_step,
-                       "arith": args.arith, "kernel": args.kernel, "parallelism": f"N-axis shard x{world}",
+            "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.describe, "id": wl.name,
+                       "tuples_per_gpu": n_real, "tuples_rank0": [data_host[0].tolist(), data_host[n_real - 1].tolist()],
+                       "configs": len(space), "evals_job_step": evals_job_step,
+                       "kernels": list(wl.kernels), "evals_per_gpu_step": evals_per_rank_step,
+                       "arith": args.arith, "kernel": args.kernel,
+                       "parallelism": f"data-tuple shard x{world} ({wl.scaling}), NCCL all-gather of winners",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_tf, "traffic": traffic,
                          "kernel": "search_kernel (fused evaluator + per-N argmin)",
-                         "flops_per_eval": statistics.mean(official_flops(specs[k]) for k in KERNELS),
+                         "flops_per_eval": statistics.mean(official_flops(specs[k]) for k in wl.kernels),
                          "kernel_ms": kernel_ms, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "rpg_search_batch (host buffers)"},
@@ -376,6 +439,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["c2", "c3", "c5"], default="c2",
+                    help="BASELINE.json config: c2 (default, configs[1]), c3 (full suite), c5 (stress)")
     ap.add_argument("--arith", choices=["exact", "fast"], default="fast")
     ap.add_argument("--kernel", choices=["specialized", "generic"], default="specialized")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

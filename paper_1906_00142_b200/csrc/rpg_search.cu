@@ -32,20 +32,20 @@ namespace {
 
 template <bool FAST>
 __global__ void __launch_bounds__(kThreads)
-generic_search(const Params P, const int64_t* __restrict__ data, int64_t n,
+generic_search(const __grid_constant__ Params P, const int64_t* __restrict__ data, int64_t n,
                rpg_winner* __restrict__ out) {
   search_body<FAST, GenericEval<FAST>>(P, data, n, out);
 }
 
 template <bool FAST>
 __global__ void __launch_bounds__(kThreads)
-generic_evaluate(const Params P, const int64_t* __restrict__ data, int64_t n,
+generic_evaluate(const __grid_constant__ Params P, const int64_t* __restrict__ data, int64_t n,
                  double* __restrict__ ec, uint8_t* __restrict__ tag,
                  int32_t* __restrict__ wocc) {
   evaluate_body<FAST, GenericEval<FAST>>(P, data, n, ec, tag, wocc);
 }
 
-__global__ void occ_table_kernel(const Params P, int4* __restrict__ occ) {
+__global__ void occ_table_kernel(const __grid_constant__ Params P, int4* __restrict__ occ) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < P.n_space) occ[c] = occ_entry(P, P.cfg[c]);
 }
