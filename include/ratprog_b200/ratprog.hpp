@@ -96,6 +96,35 @@ struct FitReport {
   bool truncated = false;
 };
 
+// Paper-artifact interop (KLARAPTOR per-metric AltArr_t polynomials,
+// PAPER.md:39-56; rpg_aa_* in rpg.h): an AltArr-form polynomial -> the
+// reference's Polynomial with terms in graded-lex basis order (the
+// evaluator's summation order).  Throws std::invalid_argument on a
+// non-canonical AltArr.
+inline Polynomial from_altarr(const rpg_altarr& a, const std::vector<std::string>& variables) {
+  if ((int)variables.size() != a.nvar)
+    throw std::invalid_argument("from_altarr: variable count does not match nvar");
+  const int cap = std::max(a.size, 1);
+  std::vector<double> c(cap);
+  std::vector<uint8_t> e((size_t)cap * std::max(a.nvar, 1));
+  int32_t n = 0;
+  char err[512] = {0};
+  if (rpg_aa_to_poly(&a, c.data(), e.data(), cap, &n, err, sizeof err) != RPG_OK)
+    throw std::invalid_argument(err);
+  Polynomial p;
+  p.variables = variables;
+  for (int k = 0; k < n; ++k) {
+    p.basis.emplace_back(e.begin() + (size_t)k * a.nvar, e.begin() + (size_t)(k + 1) * a.nvar);
+    p.coeffs.push_back(c[k]);
+  }
+  return p;
+}
+
+inline RationalFunction ratfunc_from_altarr(const rpg_altarr& num, const rpg_altarr& den,
+                                            const std::vector<std::string>& variables) {
+  return RationalFunction{from_altarr(num, variables), from_altarr(den, variables)};
+}
+
 }  // namespace poly
 
 // ---------------------------------------------------------------------------

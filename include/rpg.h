@@ -331,6 +331,56 @@ int rpg_eval_ratfunc_batch(const rpg_poly* num, const rpg_poly* den, int32_t n_v
  * std::mt19937_64(seed), in order (host). */
 int rpg_uniform_stream(uint64_t seed, int64_t n, double lo, double hi, double* out);
 
+/* ---------------------------------------------------------------------------
+ * Paper-artifact interop: KLARAPTOR ships each fitted
+ * metric as numerator / denominator polynomials in the BPAS library's
+ * sparse AltArr_t encoding (the reference itself drops it,
+ * SPEC.md:14).  rpg_altarr mirrors AltArr_t's shape — size, alloc, nvar,
+ * unpacked flag, then (coefficient, packed degrees) elements in decreasing
+ * packed-degree order — with binary64 coefficients (the fitted values the
+ * pipeline carries) instead of GMP rationals.  Degrees pack variable 0 into
+ * the most significant field: field width w = 64 / nvar bits, variable v at
+ * bits [64 - (v+1) w, 64 - v w) — so descending packed order is descending
+ * lex order with variable 0 most significant.  nvar <= RPG_MAX_VARS. */
+typedef struct {
+  double coef;
+  uint64_t degs;
+} rpg_aa_elem;
+
+typedef struct {
+  int32_t size, alloc, nvar, unpacked;
+  rpg_aa_elem* elems;
+} rpg_altarr;
+
+uint64_t rpg_aa_pack_degs(const uint8_t* exps, int32_t nvar);
+void rpg_aa_unpack_degs(uint64_t degs, int32_t nvar, uint8_t* exps);
+
+/* rpg_poly (graded-lex basis order) -> AltArr: exact-zero coefficients
+ * dropped (as emit_ratfunc does, perfmodel.hpp:521), elements sorted by
+ * decreasing packed degrees.  out->elems must hold out->alloc elements;
+ * out->size receives the term count.  RPG_E_INVALID on capacity or nvar. */
+int rpg_aa_from_poly(const rpg_poly* p, int32_t nvar, rpg_altarr* out, char* err,
+                     size_t errlen);
+
+/* AltArr -> rpg_poly arrays: terms reordered into the reference's graded-lex
+ * basis order (polyfit.hpp:50-73: ascending total degree, then lex with
+ * variable 0 most significant), which fixes the evaluator's summation order
+ * (so a model imported from AltArr evaluates bit-identically to the same
+ * model read from ratprog-models-v1 JSON).  Zero coefficients are dropped.
+ * coef[cap], exps[cap * nvar] caller-allocated; *n_terms receives the count.
+ * RPG_E_INVALID on capacity, nvar, an unsorted or duplicated monomial (not a
+ * canonical AltArr), or a non-finite coefficient. */
+int rpg_aa_to_poly(const rpg_altarr* a, double* coef, uint8_t* exps, int32_t cap,
+                   int32_t* n_terms, char* err, size_t errlen);
+
+/* C header text of one metric in the paper's per-metric-header form
+ * (PAPER.md:27-56): static rpg_aa_elem / rpg_altarr definitions
+ * `<name>_num` and `<name>_den` (coefficients as exact hex-float literals).
+ * Same buffer / return conventions as rpg_emit_cuda_source. */
+int64_t rpg_emit_altarr_header(const rpg_poly* num, const rpg_poly* den, int32_t nvar,
+                               const char* const* var_names, const char* name, char* buf,
+                               size_t buflen, char* err, size_t errlen);
+
 /* One-shot convenience for FFI callers. */
 int rpg_search(const rpg_model* model, const rpg_profile* hw,
                const rpg_config* space, int64_t n_space,

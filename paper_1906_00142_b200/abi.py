@@ -109,6 +109,15 @@ def var_kind(name: str) -> int:
     return int(name[1:]) - 1  # D<k> -> k-1
 
 
+class rpg_aa_elem(C.Structure):
+    _fields_ = [("coef", C.c_double), ("degs", C.c_uint64)]
+
+
+class rpg_altarr(C.Structure):
+    _fields_ = [("size", C.c_int32), ("alloc", C.c_int32), ("nvar", C.c_int32),
+                ("unpacked", C.c_int32), ("elems", C.POINTER(rpg_aa_elem))]
+
+
 class PackedModel:
     """An rpg_model plus the numpy buffers its pointers reference.
 
@@ -229,6 +238,14 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                              C.POINTER(C.c_double), C.POINTER(C.c_int32)) + errbuf),
         "rpg_uniform_stream": (C.c_int, (C.c_uint64, C.c_int64, C.c_double, C.c_double,
                                          C.POINTER(C.c_double))),
+        "rpg_aa_pack_degs": (C.c_uint64, (C.POINTER(C.c_uint8), C.c_int32)),
+        "rpg_aa_unpack_degs": (None, (C.c_uint64, C.c_int32, C.POINTER(C.c_uint8))),
+        "rpg_aa_from_poly": (C.c_int, (C.POINTER(rpg_poly), C.c_int32, C.POINTER(rpg_altarr)) + errbuf),
+        "rpg_aa_to_poly": (C.c_int, (C.POINTER(rpg_altarr), C.POINTER(C.c_double), C.POINTER(C.c_uint8),
+                                     C.c_int32, C.POINTER(C.c_int32)) + errbuf),
+        "rpg_emit_altarr_header": (C.c_int64, (C.POINTER(rpg_poly), C.POINTER(rpg_poly), C.c_int32,
+                                               C.POINTER(C.c_char_p), C.c_char_p, C.c_char_p,
+                                               C.c_size_t) + errbuf),
         "rpg_search": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
                                  C.POINTER(rpg_config), C.c_int64,
                                  C.POINTER(rpg_options), C.POINTER(C.c_int64),
@@ -249,7 +266,9 @@ EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_fit_rational", "rpg_program_plan_create",
                     "rpg_plan_poll_error", "rpg_emit_program_cuda_source",
                     "rpg_search_batch_subsets", "rpg_search_batch_subsets_device",
-                    "rpg_mwpcwp_cycles_batch", "rpg_eval_ratfunc_batch", "rpg_uniform_stream")
+                    "rpg_mwpcwp_cycles_batch", "rpg_eval_ratfunc_batch", "rpg_uniform_stream",
+                    "rpg_aa_pack_degs", "rpg_aa_unpack_degs", "rpg_aa_from_poly",
+                    "rpg_aa_to_poly", "rpg_emit_altarr_header")
 
 
 class RpgError(RuntimeError):

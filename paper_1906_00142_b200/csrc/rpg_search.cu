@@ -45,9 +45,16 @@ generic_evaluate(const __grid_constant__ Params P, const int64_t* __restrict__ d
   evaluate_body<FAST, GenericEval<FAST>>(P, data, n, ec, tag, wocc);
 }
 
-__global__ void occ_table_kernel(const __grid_constant__ Params P, int4* __restrict__ occ) {
+__global__ void occ_table_kernel(const __grid_constant__ Params P, int4* __restrict__ occ,
+                                 double* __restrict__ rcp) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < P.n_space) occ[c] = occ_entry(P, P.cfg[c]);
+  if (c < P.n_space) {
+    const int4 e = occ_entry(P, P.cfg[c]);
+    occ[c] = e;
+    const int b = e.x & 0xffff;
+    // RN(1 / (b * num_SM)): the repetition denominator's reciprocal (RcpDiv).
+    rcp[c] = b ? __ddiv_rn(1.0, (double)__int_as_float(e.w)) : 0.0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -122,6 +129,7 @@ struct rpg_plan {
   int32_t* d_slot_terms = nullptr;
   int4* d_cfg = nullptr;
   int4* d_occ = nullptr;
+  double* d_occ_rcp = nullptr;
   // bare-program plans: first evaluation error (Params::err_flag)
   bool is_program = false;
   long long step_limit = 0;
@@ -375,6 +383,7 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
   PLAN_CUDA(cudaMalloc(&plan->d_slot_terms, sizeof(int32_t) * std::max<size_t>(slot_terms.size(), 1)));
   PLAN_CUDA(cudaMalloc(&plan->d_cfg, sizeof(int4) * cfg.size()));
   PLAN_CUDA(cudaMalloc(&plan->d_occ, sizeof(int4) * cfg.size()));
+  PLAN_CUDA(cudaMalloc(&plan->d_occ_rcp, sizeof(double) * cfg.size()));
   PLAN_CUDA(cudaMalloc(&plan->d_err, sizeof(unsigned long long)));
   PLAN_CUDA(cudaMemset(plan->d_err, 0xff, sizeof(unsigned long long)));
   if (!coef.empty()) {
@@ -392,10 +401,11 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
   P.cfg = plan->d_cfg;
   P.n_space = (int32_t)n_space;
   P.occ = plan->d_occ;
+  P.occ_rcp = plan->d_occ_rcp;
   P.err_flag = plan->d_err;
   P.d = 0;
   if (P.occ_const) {
-    occ_table_kernel<<<(int)((n_space + 255) / 256), 256, 0, plan->stream>>>(P, plan->d_occ);
+    occ_table_kernel<<<(int)((n_space + 255) / 256), 256, 0, plan->stream>>>(P, plan->d_occ, plan->d_occ_rcp);
     PLAN_CUDA(cudaGetLastError());
     PLAN_CUDA(cudaStreamSynchronize(plan->stream));
   }
@@ -551,6 +561,7 @@ int rpg_plan_destroy(rpg_plan* plan) {
   cudaFree(plan->d_slot_terms);
   cudaFree(plan->d_cfg);
   cudaFree(plan->d_occ);
+  cudaFree(plan->d_occ_rcp);
   cudaFree(plan->d_err);
   cudaFree(plan->d_data);
   cudaFree(plan->d_out);

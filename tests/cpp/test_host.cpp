@@ -54,6 +54,28 @@ static void cpu_tests() {
   CHECK(models.models.at(perf::kMetricComp).fn.num.coeffs.size() == 27);
   perf::MetricSpec spec = pipe::to_metric_spec(models);
   CHECK(spec.constants.at(perf::kMetricRegs) == 24.0);
+  {
+    // AltArr interop: graded-lex polynomial -> AltArr -> graded-lex, zeros dropped.
+    const poly::Polynomial& p = models.models.at(perf::kMetricComp).fn.num;
+    std::vector<double> c;
+    std::vector<uint8_t> e;
+    for (size_t k = 0; k < p.coeffs.size(); ++k)
+      if (p.coeffs[k] != 0.0) {
+        c.push_back(p.coeffs[k]);
+        for (int x : p.basis[k]) e.push_back((uint8_t)x);
+      }
+    rpg_poly rp{(int32_t)c.size(), 0, c.data(), e.data()};
+    std::vector<rpg_aa_elem> el(c.size());
+    rpg_altarr aa{0, (int32_t)el.size(), 3, 0, el.data()};
+    CHECK(rpg_aa_from_poly(&rp, 3, &aa, nullptr, 0) == RPG_OK && aa.size == (int)c.size());
+    for (int i = 1; i < aa.size; ++i) CHECK(el[i].degs < el[i - 1].degs);
+    poly::Polynomial back = poly::from_altarr(aa, p.variables);
+    CHECK(back.coeffs == c);
+    for (size_t k = 0; k < back.basis.size(); ++k)
+      for (int v = 0; v < 3; ++v) CHECK(back.basis[k][v] == e[k * 3 + v]);
+    std::swap(el[0], el[1]);
+    CHECK(throws_with<std::invalid_argument>([&] { poly::from_altarr(aa, p.variables); }, "decreasing degree order"));
+  }
   CHECK(throws_with<pipe::PipelineError>([] { pipe::parse_models("{ not json"); }, "not valid JSON"));
   CHECK(throws_with<pipe::PipelineError>([] { pipe::parse_models("{\"schema\":\"other-v9\"}"); }, "ratprog-models-v1"));
   auto missing = models;
