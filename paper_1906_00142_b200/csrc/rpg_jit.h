@@ -17,6 +17,13 @@ struct Module {
   size_t cubin_bytes = 0;
 };
 
+// Threads per CTA of the specialized kernels (RPG_JIT_THREADS overrides the
+// default for tuning sweeps) and the resident CTAs per SM their register
+// budget targets (RPG_JIT_MIN_BLOCKS overrides).
+constexpr int kDefaultThreads = 256;
+int jit_threads();
+int default_min_blocks();
+
 // CUDA source of the specialized kernels for a plan's model.
 std::string generate_source(const rpg::Params& P, const std::vector<double>& coef,
                             const std::vector<uint64_t>& exps, bool fast, bool two_point = false);

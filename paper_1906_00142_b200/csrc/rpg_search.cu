@@ -121,6 +121,7 @@ struct rpg_plan {
   int max_data_index = -1;
   size_t smem = 0;
   int grid_search = 0, grid_eval = 0;
+  int threads = kThreads;  // blockDim of the search / evaluate kernels
   int sm_count = 0;
   rpg_jit::Module jit;
   double* d_coef = nullptr;
@@ -419,17 +420,16 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     std::string jerr;
     // Resident CTAs per SM the specialized kernels are register-budgeted for
     // (launch bounds); RPG_JIT_MIN_BLOCKS overrides it for tuning sweeps.
-    int min_blocks = 3;
-    if (const char* e = getenv("RPG_JIT_MIN_BLOCKS")) min_blocks = std::max(1, atoi(e));
-    if (jit(min_blocks, &plan->jit, &jerr) != 0)
+    if (jit(rpg_jit::default_min_blocks(), &plan->jit, &jerr) != 0)
       return fail(set_err(err, errlen, RPG_E_CUDA, "%s", jerr.c_str()));
+    plan->threads = rpg_jit::jit_threads();
   }
   auto setup = [&](const void* fn, int* grid) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)plan->smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, plan->smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, plan->threads, plan->smem);
     if (e != cudaSuccess) return e;
     *grid = std::max(1, per_sm) * plan->sm_count;
     return cudaSuccess;
@@ -648,7 +648,7 @@ int launch_search(rpg_plan* plan, const int64_t* d_data, int64_t n, int32_t d,
   P.sub_list = d_sub_list;
   const int grid = (int)std::min<int64_t>(n, plan->grid_search);
   void* args[] = {&P, &d_data, &n, &d_out};
-  CUDA_TRY(cudaLaunchKernel(search_fn(plan), dim3(grid), dim3(kThreads), args, plan->smem, s));
+  CUDA_TRY(cudaLaunchKernel(search_fn(plan), dim3(grid), dim3(plan->threads), args, plan->smem, s));
   return RPG_OK;
 }
 
@@ -659,7 +659,7 @@ int launch_evaluate(rpg_plan* plan, const int64_t* d_data, int64_t n, int32_t d,
   P.d = d;
   const int grid = (int)std::min<int64_t>(n, plan->grid_eval);
   void* args[] = {&P, &d_data, &n, &ec, &tag, &wocc};
-  CUDA_TRY(cudaLaunchKernel(evaluate_fn(plan), dim3(grid), dim3(kThreads), args, plan->smem, s));
+  CUDA_TRY(cudaLaunchKernel(evaluate_fn(plan), dim3(grid), dim3(plan->threads), args, plan->smem, s));
   return RPG_OK;
 }
 
