@@ -462,12 +462,38 @@ __global__ void den_colsum(const FitParams F, double* __restrict__ partial) {
 constexpr int kAlphas = 4;
 constexpr int kPassRows = 256;
 
+// Device-side control of the positivity minimizer's Newton / line-search loop
+// (positive_den_minimizer, polyfit.hpp:242-311), so the whole loop runs as a
+// stream of kernels without a host round trip per iteration.
+enum { kMinNewton = 0, kMinLine = 1, kMinDone = 2, kMinFail = 3 };
+struct MinCtl {
+  int phase, outer, inner, n_alpha;
+  double mu, phi0, decrement, alpha;  // alpha: first candidate of the next line pass
+  double al[kAlphas];
+};
+// Candidate source of a controlled den_pass: c, dc in equilibrated
+// coordinates, S the column scale.
+struct CtlSrc {
+  const MinCtl* ctl;
+  const double* c;
+  const double* dc;
+  const double* S;
+};
+
 __global__ void __launch_bounds__(kFitThreads)
 den_pass(const FitParams F, const double* __restrict__ cd, const double* __restrict__ dd,
          const double* __restrict__ alphas, int n_alpha, int newton,
-         double* __restrict__ partial /* per block: 2*kAlphas + nd + nd*nd */) {
+         double* __restrict__ partial /* per block: 2*kAlphas + nd + nd*nd */, CtlSrc src) {
   extern __shared__ __align__(16) double fsm[];
   const int nd = F.nd;
+  if (src.ctl) {
+    // Controlled pass: NEWTON = candidate S.*c (with the Newton sums), LINE =
+    // S.*c + al[a] (S.*dc) for the pass's candidates; nothing once finished.
+    const int ph = src.ctl->phase;
+    if (ph >= kMinDone) return;
+    newton = ph == kMinNewton;
+    n_alpha = newton ? 1 : src.ctl->n_alpha;
+  }
   double* U = fsm;                                  // kPassRows x nd (row-major)
   double* red = U + kPassRows * kMaxCols;           // 32
   double* cands = red + 32;                         // kAlphas x nd
@@ -476,7 +502,13 @@ den_pass(const FitParams F, const double* __restrict__ cd, const double* __restr
     sexps[e] = F.exps[F.nn * F.n_vars + e];
   for (int e = threadIdx.x; e < n_alpha * nd; e += blockDim.x) {
     const int a = e / nd, k = e % nd;
-    cands[e] = dd ? cd[k] + alphas[a] * dd[k] : cd[k];
+    if (src.ctl) {
+      const int j = F.nn + k;
+      const double ck = src.S[j] * src.c[j];
+      cands[e] = newton ? ck : ck + src.ctl->al[a] * (src.S[j] * src.dc[j]);
+    } else {
+      cands[e] = dd ? cd[k] + alphas[a] * dd[k] : cd[k];
+    }
   }
   __syncthreads();
   double qmin[kAlphas], slog[kAlphas];
@@ -561,13 +593,19 @@ den_pass(const FitParams F, const double* __restrict__ cd, const double* __restr
 
 // Sums the per-block partials of den_pass (min for the q minima).
 __global__ void den_pass_final(const double* __restrict__ partial, int G, int nd,
-                               double* __restrict__ out) {
+                               double* __restrict__ out, const MinCtl* __restrict__ ctl) {
+  if (ctl && ctl->phase >= kMinDone) return;
   const int W = 2 * kAlphas + nd + nd * nd;
-  for (int e = threadIdx.x; e < W; e += blockDim.x) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int e = warp; e < W; e += nw) {
     const bool is_min = e < 2 * kAlphas && (e % 2) == 0;
     double t = is_min ? INFINITY : 0.0;
-    for (int g = 0; g < G; ++g) t = is_min ? fmin(t, partial[(size_t)g * W + e]) : t + partial[(size_t)g * W + e];
-    out[e] = t;
+    for (int g = lane; g < G; g += 32) t = is_min ? fmin(t, partial[(size_t)g * W + e]) : t + partial[(size_t)g * W + e];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, t, o);
+      t = is_min ? fmin(t, u) : t + u;
+    }
+    if (lane == 0) out[e] = t;
   }
 }
 
@@ -582,7 +620,7 @@ __device__ double rs_norm2(const double* R, const double* S, const double* v, in
   return acc;
 }
 
-// Minimizer state (device): c (n, equilibrated coordinates), dc (n), scalars.
+// Setup state of the minimizer (min_setup).
 struct MinState {
   double mu, phi0, decrement;
   int ok;
@@ -610,32 +648,20 @@ __global__ void min_setup(const double* __restrict__ R, const double* __restrict
   st->ok = 1;
 }
 
-// Raw-coordinate denominator coefficients (S_den .* c_den) and direction.
-__global__ void raw_den(const double* __restrict__ c, const double* __restrict__ dc,
-                        const double* __restrict__ S, int nn, int nd, double* __restrict__ cd,
-                        double* __restrict__ dd) {
-  for (int k = threadIdx.x; k < nd; k += blockDim.x) {
-    cd[k] = S[nn + k] * c[nn + k];
-    if (dc && dd) dd[k] = S[nn + k] * dc[nn + k];
-  }
-}
-
 // Newton step: grad = 2 H0 c - mu Q^T(1/q), H = 2 H0 + mu Q^T diag(1/q^2) Q,
 // KKT [H g; g^T 0] [dc; l] = [-grad; 0] solved by Gaussian elimination with
 // partial pivoting (the reference uses LDLT), decrement = -grad.dc,
 // phi0 = ||A_eq c||^2 - mu sum log q.  One CTA.
-__global__ void __launch_bounds__(kFitThreads)
-newton_step(const double* __restrict__ R, const double* __restrict__ S,
-            const double* __restrict__ gsum, const double* __restrict__ pass_out,
-            const double* __restrict__ c, int nn, int nd, double* __restrict__ dc,
-            MinState* __restrict__ st) {
+__device__ void newton_body(const double* __restrict__ R, const double* __restrict__ S,
+                            const double* __restrict__ gsum, const double* __restrict__ pass_out,
+                            const double* __restrict__ c, int nn, int nd, double* __restrict__ dc,
+                            const double mu, MinState* __restrict__ st) {
   extern __shared__ __align__(16) double fsm[];
   const int n = nn + nd, N = n + 1;
   double* K = fsm;                 // N x (N+1) augmented, row-major
   double* H0c = K + N * (N + 1);   // n
   double* RSc = H0c + n;           // n: (R S c)
   double* grad = RSc + n;          // n
-  const double mu = st->mu;
   const double* gq = pass_out + 2 * kAlphas;
   const double* G = gq + nd;
   // RSc = R S c
@@ -732,21 +758,97 @@ newton_step(const double* __restrict__ R, const double* __restrict__ S,
   }
 }
 
-// phi(c + alpha dc) for the candidate alphas: ||R S cn||^2 - mu sum log qn.
-__global__ void line_phi(const double* __restrict__ R, const double* __restrict__ S,
-                         const double* __restrict__ c, const double* __restrict__ dc,
-                         const double* __restrict__ alphas, int n_alpha, int n,
-                         const double* __restrict__ pass_out, const MinState* __restrict__ st,
-                         double* __restrict__ phis) {
-  const int a = threadIdx.x;
-  if (a >= n_alpha) return;
-  double cn[kMaxCols];
-  for (int k = 0; k < n; ++k) cn[k] = c[k] + alphas[a] * dc[k];
-  phis[a] = rs_norm2(R, S, cn, n) - st->mu * pass_out[2 * a + 1];
+// The inner loop ended (no decrement, no acceptable step, or 40 steps):
+// mu *= 0.1 and the next outer round (16 rounds).
+__device__ __forceinline__ void ctl_end_inner(MinCtl* ctl) {
+  ctl->mu *= 0.1;
+  ctl->outer += 1;
+  ctl->inner = 0;
+  ctl->phase = ctl->outer >= 16 ? kMinDone : kMinNewton;
 }
 
-__global__ void axpy_small(double* __restrict__ c, const double* __restrict__ dc, double alpha, int n) {
-  for (int k = threadIdx.x; k < n; k += blockDim.x) c[k] += alpha * dc[k];
+// One controlled step after its den_pass (pass_out):
+//   NEWTON: the KKT Newton direction (newton_step's algebra); stop the inner
+//           loop when the decrement is negligible, else start a line search
+//           at alpha = 1;
+//   LINE:   phi at the pass's candidates (||R S cn||^2 - mu sum log qn);
+//           accept the first (in halving order) with q > 0 and Armijo
+//           decrease, else continue halving (the inner loop ends when alpha
+//           drops to 1e-18) — polyfit.hpp:279-306.
+__global__ void __launch_bounds__(kFitThreads)
+ctl_step(const double* __restrict__ R, const double* __restrict__ S,
+         const double* __restrict__ gsum, const double* __restrict__ pass_out,
+         double* __restrict__ c, int nn, int nd, double* __restrict__ dc,
+         MinCtl* __restrict__ ctl, MinState* __restrict__ scratch) {
+  const int ph = ctl->phase;
+  if (ph >= kMinDone) return;
+  const int n = nn + nd;
+  if (ph == kMinNewton) {
+    newton_body(R, S, gsum, pass_out, c, nn, nd, dc, ctl->mu, scratch);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (!scratch->ok) {
+        ctl->phase = kMinFail;  // non-finite KKT solution: empty result
+      } else if (!(scratch->decrement > 1e-14 * (1.0 + fabs(scratch->phi0)))) {
+        ctl_end_inner(ctl);
+      } else {
+        ctl->phi0 = scratch->phi0;
+        ctl->decrement = scratch->decrement;
+        ctl->phase = kMinLine;
+        ctl->alpha = 1.0;
+        int na = 0;
+        for (double a = 1.0; na < kAlphas && a > 1e-18; a *= 0.5) ctl->al[na++] = a;
+        ctl->n_alpha = na;
+      }
+    }
+    return;
+  }
+  // LINE: phis of the candidates, one warp each.
+  __shared__ double phis[kAlphas];
+  __shared__ int accepted;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int na = ctl->n_alpha;
+  if (warp < na) {
+    const double al = ctl->al[warp];
+    double acc = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      double t = 0.0;
+      for (int k = i; k < n; ++k) t = fma(R[i * n + k], S[k] * (c[k] + al * dc[k]), t);
+      acc = fma(t, t, acc);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) phis[warp] = acc - ctl->mu * pass_out[2 * warp + 1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    accepted = -1;
+    for (int a = 0; a < na; ++a)
+      if (pass_out[2 * a] > 0.0 && phis[a] <= ctl->phi0 - 1e-4 * ctl->al[a] * ctl->decrement) {
+        accepted = a;
+        break;
+      }
+  }
+  __syncthreads();
+  if (accepted >= 0) {
+    const double al = ctl->al[accepted];
+    for (int k = threadIdx.x; k < n; k += blockDim.x) c[k] += al * dc[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ctl->inner += 1;
+      if (ctl->inner >= 40) ctl_end_inner(ctl);
+      else ctl->phase = kMinNewton;
+    }
+  } else if (threadIdx.x == 0) {
+    const double next = ctl->al[na - 1] * 0.5;
+    if (!(next > 1e-18)) {
+      ctl_end_inner(ctl);  // no acceptable step: break the inner loop
+    } else {
+      int k = 0;
+      for (double a = next; k < kAlphas && a > 1e-18; a *= 0.5) ctl->al[k++] = a;
+      ctl->n_alpha = k;
+      ctl->alpha = next;
+    }
+  }
 }
 
 __global__ void to_raw(const double* __restrict__ c, const double* __restrict__ S, int n,
@@ -926,7 +1028,7 @@ struct Pass {
 
 int run_den_pass(const FitParams& F, const double* cd, const double* dd, const double* alphas,
                  int n_alpha, int newton, int sms, Pass* P, cudaStream_t s, char* err,
-                 size_t errlen) {
+                 size_t errlen, CtlSrc src = CtlSrc{nullptr, nullptr, nullptr, nullptr}) {
   const int W = 2 * kAlphas + F.nd + F.nd * F.nd;
   if (!P->part.p) {
     const int64_t tiles = (F.m + kPassRows - 1) / kPassRows;
@@ -938,9 +1040,9 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
   const size_t sm = sizeof(double) * ((size_t)kPassRows * kMaxCols + 32 + kAlphas * kMaxCols) +
                     (size_t)kMaxCols * RPG_MAX_VARS + 16;
   FCUDA(cudaFuncSetAttribute(den_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  den_pass<<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>());
+  den_pass<<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>(), src);
   FCUDA(cudaGetLastError());
-  den_pass_final<<<1, 256, 0, s>>>(P->part.as<double>(), P->G, F.nd, P->out.as<double>());
+  den_pass_final<<<1, 256, 0, s>>>(P->part.as<double>(), P->G, F.nd, P->out.as<double>(), src.ctl);
   return RPG_OK;
 }
 
@@ -953,14 +1055,11 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
               char* err, size_t errlen) {
   const int nn = F.nn, nd = F.nd, n = F.n;
   *found = 0;
-  DevBuf c, dc, cd, dd, alphas, st, phis, fin;
+  DevBuf c, dc, cd, st, fin;
   FCUDA(cudaMalloc(&c.p, sizeof(double) * n));
   FCUDA(cudaMalloc(&dc.p, sizeof(double) * n));
   FCUDA(cudaMalloc(&cd.p, sizeof(double) * nd));
-  FCUDA(cudaMalloc(&dd.p, sizeof(double) * nd));
-  FCUDA(cudaMalloc(&alphas.p, sizeof(double) * kAlphas));
   FCUDA(cudaMalloc(&st.p, sizeof(MinState)));
-  FCUDA(cudaMalloc(&phis.p, sizeof(double) * kAlphas));
   FCUDA(cudaMalloc(&fin.p, sizeof(int)));
   Pass P;
   // q of the start vector: Q (start / S) = D start_den.
@@ -973,55 +1072,34 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   FCUDA(cudaMemcpyAsync(&hs, st.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
   FCUDA(cudaStreamSynchronize(s));
   if (!hs.ok) return RPG_OK;
-  double mu = hs.mu;
   const size_t smk = sizeof(double) * ((size_t)(kMaxCols + 1) * (kMaxCols + 2) + 3 * kMaxCols);
-  FCUDA(cudaFuncSetAttribute(newton_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smk));
-  for (int outer = 0; outer < 16; ++outer) {
-    for (int inner = 0; inner < 40; ++inner) {
-      raw_den<<<1, 64, 0, s>>>(c.as<double>(), nullptr, S, nn, nd, cd.as<double>(), nullptr);
-      rc = run_den_pass(F, cd.as<double>(), nullptr, nullptr, 1, 1, sms, &P, s, err, errlen);
+  FCUDA(cudaFuncSetAttribute(ctl_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smk));
+  DevBuf ctlb;
+  FCUDA(cudaMalloc(&ctlb.p, sizeof(MinCtl)));
+  MinCtl hc{};
+  hc.phase = kMinNewton;
+  hc.mu = hs.mu;
+  hc.n_alpha = 1;
+  FCUDA(cudaMemcpyAsync(ctlb.p, &hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+  MinCtl* dctl = ctlb.as<MinCtl>();
+  const CtlSrc src{dctl, c.as<double>(), dc.as<double>(), S};
+  // Steps (controlled den_pass + reduction + Newton-or-line update) are
+  // enqueued in chunks; the host only polls the phase between chunks.
+  // Bound: 16 outer x 40 inner x (1 Newton + <= 15 line passes).
+  constexpr int kChunk = 24;
+  for (int done = 0, steps = 0; !done && steps < 16 * 40 * 16; steps += kChunk) {
+    for (int i = 0; i < kChunk; ++i) {
+      rc = run_den_pass(F, nullptr, nullptr, nullptr, 1, 1, sms, &P, s, err, errlen, src);
       if (rc) return rc;
-      newton_step<<<1, kFitThreads, smk, s>>>(R, S, gsum, P.out.as<double>(), c.as<double>(), nn,
-                                               nd, dc.as<double>(), st.as<MinState>());
-      FCUDA(cudaGetLastError());
-      FCUDA(cudaMemcpyAsync(&hs, st.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
-      FCUDA(cudaStreamSynchronize(s));
-      if (!hs.ok) return RPG_OK;  // non-finite KKT solution: empty result
-      if (!(hs.decrement > 1e-14 * (1.0 + std::fabs(hs.phi0)))) break;
-      bool stepped = false;
-      double alpha = 1.0;
-      raw_den<<<1, 64, 0, s>>>(c.as<double>(), dc.as<double>(), S, nn, nd, cd.as<double>(),
-                               dd.as<double>());
-      while (alpha > 1e-18 && !stepped) {
-        double al[kAlphas];
-        int na = 0;
-        for (double a = alpha; na < kAlphas && a > 1e-18; a *= 0.5) al[na++] = a;
-        FCUDA(cudaMemcpyAsync(alphas.p, al, sizeof(double) * na, cudaMemcpyHostToDevice, s));
-        rc = run_den_pass(F, cd.as<double>(), dd.as<double>(), alphas.as<double>(), na, 0, sms, &P,
-                          s, err, errlen);
-        if (rc) return rc;
-        line_phi<<<1, 32, 0, s>>>(R, S, c.as<double>(), dc.as<double>(), alphas.as<double>(), na, n,
-                                  P.out.as<double>(), st.as<MinState>(), phis.as<double>());
-        double po[2 * kAlphas], ph[kAlphas];
-        FCUDA(cudaMemcpyAsync(po, P.out.p, sizeof(po), cudaMemcpyDeviceToHost, s));
-        FCUDA(cudaMemcpyAsync(ph, phis.p, sizeof(double) * na, cudaMemcpyDeviceToHost, s));
-        FCUDA(cudaStreamSynchronize(s));
-        for (int a = 0; a < na; ++a) {
-          if (po[2 * a] > 0.0 && ph[a] <= hs.phi0 - 1e-4 * al[a] * hs.decrement) {
-            axpy_small<<<1, 64, 0, s>>>(c.as<double>(), dc.as<double>(), al[a], n);
-            stepped = true;
-            break;
-          }
-        }
-        alpha = al[na - 1] * 0.5;
-      }
-      if (!stepped) break;
+      ctl_step<<<1, kFitThreads, smk, s>>>(R, S, gsum, P.out.as<double>(), c.as<double>(), nn, nd,
+                                           dc.as<double>(), dctl, st.as<MinState>());
     }
-    mu *= 0.1;
-    MinState upd = hs;
-    upd.mu = mu;
-    FCUDA(cudaMemcpyAsync(st.p, &upd, sizeof(upd), cudaMemcpyHostToDevice, s));
+    FCUDA(cudaGetLastError());
+    FCUDA(cudaMemcpyAsync(&hc, ctlb.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    FCUDA(cudaStreamSynchronize(s));
+    done = hc.phase >= kMinDone;
   }
+  if (hc.phase == kMinFail) return RPG_OK;
   to_raw<<<1, 32, 0, s>>>(c.as<double>(), S, n, out_raw, fin.as<int>());
   int f = 0;
   FCUDA(cudaMemcpyAsync(&f, fin.p, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -20,7 +20,7 @@ struct Module {
 // Threads per CTA of the specialized kernels (RPG_JIT_THREADS overrides the
 // default for tuning sweeps) and the resident CTAs per SM their register
 // budget targets (RPG_JIT_MIN_BLOCKS overrides).
-constexpr int kDefaultThreads = 256;
+constexpr int kDefaultThreads = 32;
 int jit_threads();
 int default_min_blocks();
 

@@ -46,14 +46,25 @@ generic_evaluate(const __grid_constant__ Params P, const int64_t* __restrict__ d
 }
 
 __global__ void occ_table_kernel(const __grid_constant__ Params P, int4* __restrict__ occ,
-                                 double* __restrict__ rcp) {
+                                 double* __restrict__ rcp, int4* __restrict__ lean,
+                                 double2* __restrict__ rep_tab) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < P.n_space) {
-    const int4 e = occ_entry(P, P.cfg[c]);
+    const int4 cf = P.cfg[c];
+    const int4 e = occ_entry(P, cf);
     occ[c] = e;
     const int b = e.x & 0xffff;
     // RN(1 / (b * num_SM)): the repetition denominator's reciprocal (RcpDiv).
     rcp[c] = b ? __ddiv_rn(1.0, (double)__int_as_float(e.w)) : 0.0;
+    if (lean) {
+      const int W = (int)((unsigned)e.x >> 16), bd = e.y & 0xffff, Wd = (int)((unsigned)e.y >> 16);
+      lean[c] = make_int4(cf.x | (cf.y << 16), cf.z | (b << 16), (int)((unsigned)W | ((unsigned)Wd << 16)),
+                          (bd == b && Wd == W) ? 1 : 0);
+    }
+  }
+  if (rep_tab && c <= P.hw.B_max) {
+    const double d = (double)c * (double)P.hw.num_SM;
+    rep_tab[c] = make_double2(d, c ? __ddiv_rn(1.0, d) : 0.0);
   }
 }
 
@@ -131,6 +142,8 @@ struct rpg_plan {
   int4* d_cfg = nullptr;
   int4* d_occ = nullptr;
   double* d_occ_rcp = nullptr;
+  int4* d_lean = nullptr;
+  double2* d_rep_tab = nullptr;
   // bare-program plans: first evaluation error (Params::err_flag)
   bool is_program = false;
   long long step_limit = 0;
@@ -317,6 +330,14 @@ int prepare_model(const rpg_model* model, const rpg_profile* hw, const rpg_optio
   return RPG_OK;
 }
 
+// The compact per-config record path of the specialized search kernels
+// applies when occupancy is per-config (constant regs/shared) and the
+// per-b repetition table is small; the block dimensions must also fit 16-bit
+// fields (checked against the space in build_plan).
+bool lean_eligible(const Params& P) {
+  return P.occ_const && P.hw.B_max <= 1024 && P.hw.W_max <= 0xffff;
+}
+
 int check_space(const rpg_config* space, int64_t n_space, char* err, size_t errlen) {
   if (n_space <= 0 || !space)
     return set_err(err, errlen, RPG_E_INVALID, "search_optimal: configuration space is empty");
@@ -385,6 +406,19 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
   PLAN_CUDA(cudaMalloc(&plan->d_cfg, sizeof(int4) * cfg.size()));
   PLAN_CUDA(cudaMalloc(&plan->d_occ, sizeof(int4) * cfg.size()));
   PLAN_CUDA(cudaMalloc(&plan->d_occ_rcp, sizeof(double) * cfg.size()));
+  // Compact records of the specialized search pass: block dimensions and
+  // occupancy must fit 16-bit fields, and the per-b repetition table SMEM.
+  P.lean_ok = 0;
+  if (specialized && !is_program && lean_eligible(P)) {
+    bool fits = true;
+    for (const int4& c : cfg) fits = fits && c.x >= 0 && c.x <= 0xffff && c.y >= 0 && c.y <= 0x7fff &&
+                                     c.z >= 0 && c.z <= 0xffff;
+    P.lean_ok = fits ? 1 : 0;
+  }
+  if (P.lean_ok) {
+    PLAN_CUDA(cudaMalloc(&plan->d_lean, sizeof(int4) * cfg.size()));
+    PLAN_CUDA(cudaMalloc(&plan->d_rep_tab, sizeof(double2) * (size_t)(P.hw.B_max + 1)));
+  }
   PLAN_CUDA(cudaMalloc(&plan->d_err, sizeof(unsigned long long)));
   PLAN_CUDA(cudaMemset(plan->d_err, 0xff, sizeof(unsigned long long)));
   if (!coef.empty()) {
@@ -403,15 +437,19 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
   P.n_space = (int32_t)n_space;
   P.occ = plan->d_occ;
   P.occ_rcp = plan->d_occ_rcp;
+  P.lean = plan->d_lean;
+  P.rep_tab = plan->d_rep_tab;
   P.err_flag = plan->d_err;
   P.d = 0;
   if (P.occ_const) {
-    occ_table_kernel<<<(int)((n_space + 255) / 256), 256, 0, plan->stream>>>(P, plan->d_occ, plan->d_occ_rcp);
+    const int64_t nthr = std::max<int64_t>(n_space, P.lean_ok ? P.hw.B_max + 1 : 0);
+    occ_table_kernel<<<(int)((nthr + 255) / 256), 256, 0, plan->stream>>>(
+        P, plan->d_occ, plan->d_occ_rcp, plan->d_lean, plan->d_rep_tab);
     PLAN_CUDA(cudaGetLastError());
     PLAN_CUDA(cudaStreamSynchronize(plan->stream));
   }
 
-  plan->smem = smem_layout(P.n_terms, P.n_slots).total;
+  plan->smem = smem_layout(smem_terms(P), P.n_slots, rep_entries(P)).total;
   int smem_optin = 0;
   PLAN_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   if (plan->smem > (size_t)smem_optin)
@@ -562,6 +600,8 @@ int rpg_plan_destroy(rpg_plan* plan) {
   cudaFree(plan->d_cfg);
   cudaFree(plan->d_occ);
   cudaFree(plan->d_occ_rcp);
+  cudaFree(plan->d_lean);
+  cudaFree(plan->d_rep_tab);
   cudaFree(plan->d_err);
   cudaFree(plan->d_data);
   cudaFree(plan->d_out);
@@ -842,6 +882,7 @@ extern "C" int64_t rpg_emit_cuda_source(const rpg_model* model, const rpg_profil
   ModelTables tab;
   int rc = prepare_model(model, hw, opts, P, tab, err, errlen);
   if (rc) return rc;
+  P.lean_ok = opts->kernel == RPG_KERNEL_SPECIALIZED && lean_eligible(P);  // as for a plan whose space fits
   const std::string src =
       rpg_jit::generate_source(P, tab.coef, tab.exps, opts->arith == RPG_ARITH_FAST,
                                getenv("RPG_JIT_ILP") && atoi(getenv("RPG_JIT_ILP")) == 2);
@@ -853,7 +894,7 @@ extern "C" int64_t rpg_emit_cuda_source(const rpg_model* model, const rpg_profil
   if (compile) {
     std::vector<char> cubin;
     std::string log;
-    if (rpg_jit::compile(src, 2, &cubin, &log) != 0)
+    if (rpg_jit::compile(src, rpg_jit::default_min_blocks(), &cubin, &log) != 0)
       return set_err(err, errlen, RPG_E_CUDA, "NVRTC: %s", log.substr(0, 1500).c_str());
     if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
   }
@@ -879,7 +920,7 @@ extern "C" int64_t rpg_emit_program_cuda_source(const rpg_program* prog, const r
   if (compile) {
     std::vector<char> cubin;
     std::string log;
-    if (rpg_jit::compile(src, 2, &cubin, &log) != 0)
+    if (rpg_jit::compile(src, rpg_jit::default_min_blocks(), &cubin, &log) != 0)
       return set_err(err, errlen, RPG_E_CUDA, "NVRTC: %s", log.substr(0, 1500).c_str());
     if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
   }
