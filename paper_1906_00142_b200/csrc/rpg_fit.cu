@@ -156,9 +156,9 @@ __global__ void __launch_bounds__(kFitThreads)
 tsqr_tiles(const FitParams F, double* __restrict__ Rout) {
   extern __shared__ __align__(16) double fsm[];
   const int ncols = F.num_only ? F.nn + F.with_y_col : F.n;
-  double* R = fsm;                        // kMaxCols^2
-  double* T = R + kMaxCols * kMaxCols;    // kTile * kMaxCols
-  double* red = T + kTile * kMaxCols;     // 32
+  double* R = fsm;                        // ncols^2
+  double* T = R + ncols * ncols;          // kTile * ncols
+  double* red = T + kTile * ncols;        // 32
   double* wbuf = red + 32;                // kMaxCols
   uint8_t* sexps = reinterpret_cast<uint8_t*>(wbuf + kMaxCols);
   for (int e = threadIdx.x; e < F.n * F.n_vars; e += blockDim.x) sexps[e] = F.exps[e];
@@ -175,17 +175,22 @@ tsqr_tiles(const FitParams F, double* __restrict__ Rout) {
   for (int e = threadIdx.x; e < ncols * ncols; e += blockDim.x) out[e] = R[e];
 }
 
-// K3b: R[2b] <- qr([R[2b]; R[2b+1]]).R for b < count/2 (tree level).
+// K3b: one tree level, Rout[b] <- qr([Rin[2b]; Rin[2b+1]]).R (Rin[2b] alone
+// when 2b+1 is past the level) — ping-pong buffers, no compaction copies.
 __global__ void __launch_bounds__(kFitThreads)
-tsqr_combine(double* __restrict__ Rs, int count, int n) {
+tsqr_combine(const double* __restrict__ Rs, int count, int n, double* __restrict__ Rout) {
   extern __shared__ __align__(16) double fsm[];
   double* R = fsm;
-  double* T = R + kMaxCols * kMaxCols;
-  double* red = T + kMaxCols * kMaxCols;
+  double* T = R + n * n;
+  double* red = T + n * n;
   double* wbuf = red + 32;
   const int a = 2 * blockIdx.x, b = a + 1;
-  if (b >= count) return;
   const double* Ra = Rs + (size_t)a * n * n;
+  double* out = Rout + (size_t)blockIdx.x * n * n;
+  if (b >= count) {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) out[e] = Ra[e];
+    return;
+  }
   const double* Rb = Rs + (size_t)b * n * n;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     R[e] = Ra[e];
@@ -195,7 +200,6 @@ tsqr_combine(double* __restrict__ Rs, int count, int n) {
   __syncthreads();
   fold_tile(R, T, n, n, n, red, wbuf);
   __syncthreads();
-  double* out = Rs + (size_t)a * n * n;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) out[e] = R[e];
 }
 
@@ -480,6 +484,9 @@ struct CtlSrc {
   const double* S;
 };
 
+// NDT: compile-time bound on nd (8 = the default (1,1,1) denominator basis)
+// so the per-row monomials and accumulators stay in registers.
+template <int NDT>
 __global__ void __launch_bounds__(kFitThreads)
 den_pass(const FitParams F, const double* __restrict__ cd, const double* __restrict__ dd,
          const double* __restrict__ alphas, int n_alpha, int newton,
@@ -495,9 +502,9 @@ den_pass(const FitParams F, const double* __restrict__ cd, const double* __restr
     n_alpha = newton ? 1 : src.ctl->n_alpha;
   }
   double* U = fsm;                                  // kPassRows x nd (row-major)
-  double* red = U + kPassRows * kMaxCols;           // 32
+  double* red = U + kPassRows * nd;                 // 32
   double* cands = red + 32;                         // kAlphas x nd
-  uint8_t* sexps = reinterpret_cast<uint8_t*>(cands + kAlphas * kMaxCols);
+  uint8_t* sexps = reinterpret_cast<uint8_t*>(cands + kAlphas * nd);
   for (int e = threadIdx.x; e < nd * F.n_vars; e += blockDim.x)
     sexps[e] = F.exps[F.nn * F.n_vars + e];
   for (int e = threadIdx.x; e < n_alpha * nd; e += blockDim.x) {
@@ -512,28 +519,42 @@ den_pass(const FitParams F, const double* __restrict__ cd, const double* __restr
   }
   __syncthreads();
   double qmin[kAlphas], slog[kAlphas];
+#pragma unroll
   for (int a = 0; a < kAlphas; ++a) {
     qmin[a] = INFINITY;
     slog[a] = 0.0;
   }
-  // Gram accumulators: thread t owns entries t, t+blockDim, ... of nd x nd
-  double gacc[16];
-  for (int i = 0; i < 16; ++i) gacc[i] = 0.0;
+  // Gram accumulators: with nd*nd <= blockDim/2 every entry gets `parts`
+  // threads (thread = part * nd*nd + entry); else thread t owns entries t,
+  // t + blockDim, ...
+  const int parts = (nd * nd <= (int)blockDim.x / 2) ? (int)blockDim.x / (nd * nd) >= 4 ? 4 : 2 : 1;
+  const int ne_stride = parts > 1 ? nd * nd : (int)blockDim.x;
+  const int part = parts > 1 ? (int)threadIdx.x / (nd * nd) : 0;
+  double gacc[NDT <= 8 ? 1 : 16];
+#pragma unroll
+  for (int i = 0; i < (NDT <= 8 ? 1 : 16); ++i) gacc[i] = 0.0;
   double gq = 0.0;  // thread t < nd owns sum (1/q) D[t]
   const int64_t nrow_tiles = (F.m + kPassRows - 1) / kPassRows;
   for (int64_t tile = blockIdx.x; tile < nrow_tiles; tile += gridDim.x) {
     const int64_t r = tile * kPassRows + threadIdx.x;
     const bool valid = threadIdx.x < kPassRows && r < F.m;
-    double D[kMaxCols];
+    double D[NDT];
     if (valid) {
       double x[RPG_MAX_VARS];
-      for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
-      for (int k = 0; k < nd; ++k) D[k] = monomial(x, sexps + k * F.n_vars, F.n_vars);
-      for (int a = 0; a < n_alpha; ++a) {
-        double q = 0.0;
-        for (int k = 0; k < nd; ++k) q = fma(D[k], cands[a * nd + k], q);
-        qmin[a] = fmin(qmin[a], q);
-        slog[a] += log(q);
+#pragma unroll
+      for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
+#pragma unroll
+      for (int k = 0; k < NDT; ++k) D[k] = k < nd ? monomial(x, sexps + k * F.n_vars, F.n_vars) : 0.0;
+#pragma unroll
+      for (int a = 0; a < kAlphas; ++a) {
+        if (a < n_alpha) {
+          double q = 0.0;
+#pragma unroll
+          for (int k = 0; k < NDT; ++k)
+            if (k < nd) q = fma(D[k], cands[a * nd + k], q);
+          qmin[a] = fmin(qmin[a], q);
+          slog[a] += log(q);
+        }
       }
     }
     if (newton) {
@@ -541,27 +562,58 @@ den_pass(const FitParams F, const double* __restrict__ cd, const double* __restr
       if (threadIdx.x < kPassRows) {
         double q = 0.0, qi = 0.0;
         if (valid) {
-          for (int k = 0; k < nd; ++k) q = fma(D[k], cands[k], q);
+#pragma unroll
+          for (int k = 0; k < NDT; ++k)
+            if (k < nd) q = fma(D[k], cands[k], q);
           qi = 1.0 / q;
         }
-        for (int k = 0; k < nd; ++k) U[threadIdx.x * nd + k] = valid ? D[k] * qi : 0.0;
+#pragma unroll
+        for (int k = 0; k < NDT; ++k)
+          if (k < nd) U[threadIdx.x * nd + k] = valid ? D[k] * qi : 0.0;
       }
       __syncthreads();
-      for (int e = threadIdx.x, i = 0; e < nd * nd; e += blockDim.x, ++i) {
+      // Gram of the tile's U rows: `parts` threads per entry, each over a
+      // contiguous row range with four independent accumulators.
+      for (int e = threadIdx.x % ne_stride, i = 0; part < parts && e < nd * nd; e += ne_stride, ++i) {
         const int a = e / nd, b = e % nd;
-        double t = 0.0;
-        for (int row = 0; row < kPassRows; ++row) t = fma(U[row * nd + a], U[row * nd + b], t);
-        gacc[i] += t;
+        const int r0 = part * (kPassRows / parts), r1 = r0 + kPassRows / parts;
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+        for (int row = r0; row < r1; row += 4) {
+          t0 = fma(U[row * nd + a], U[row * nd + b], t0);
+          t1 = fma(U[(row + 1) * nd + a], U[(row + 1) * nd + b], t1);
+          t2 = fma(U[(row + 2) * nd + a], U[(row + 2) * nd + b], t2);
+          t3 = fma(U[(row + 3) * nd + a], U[(row + 3) * nd + b], t3);
+        }
+        if (NDT <= 8) gacc[0] += (t0 + t1) + (t2 + t3);
+        else gacc[i] += (t0 + t1) + (t2 + t3);
       }
       if ((int)threadIdx.x < nd) {
         // sum_k (1/q_k) D_k[t] = sum of column t of U
-        double t = 0.0;
-        for (int row = 0; row < kPassRows; ++row) t += U[row * nd + threadIdx.x];
-        gq += t;
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+        for (int row = 0; row < kPassRows; row += 4) {
+          t0 += U[row * nd + threadIdx.x];
+          t1 += U[(row + 1) * nd + threadIdx.x];
+          t2 += U[(row + 2) * nd + threadIdx.x];
+          t3 += U[(row + 3) * nd + threadIdx.x];
+        }
+        gq += (t0 + t1) + (t2 + t3);
       }
     }
   }
+  if (newton && parts > 1) {
+    // Fold the per-part partial Gram entries (thread = part * ne + entry).
+    __syncthreads();
+    double* P = U;  // reuse: parts x nd*nd
+    if (threadIdx.x < parts * nd * nd) P[threadIdx.x] = gacc[0];
+    __syncthreads();
+    if ((int)threadIdx.x < nd * nd) {
+      double t = 0.0;
+      for (int q = 0; q < parts; ++q) t += P[q * nd * nd + threadIdx.x];
+      gacc[0] = t;
+    }
+  }
   double* out = partial + (size_t)blockIdx.x * (2 * kAlphas + nd + nd * nd);
+#pragma unroll
   for (int a = 0; a < kAlphas; ++a) {
     double t = qmin[a], u = slog[a];
     for (int o = 16; o > 0; o >>= 1) {
@@ -586,8 +638,12 @@ den_pass(const FitParams F, const double* __restrict__ cd, const double* __restr
   }
   if (newton) {
     if ((int)threadIdx.x < nd) out[2 * kAlphas + threadIdx.x] = gq;
-    for (int e = threadIdx.x, i = 0; e < nd * nd; e += blockDim.x, ++i)
-      out[2 * kAlphas + nd + e] = gacc[i];
+    if (parts > 1) {
+      if ((int)threadIdx.x < nd * nd) out[2 * kAlphas + nd + threadIdx.x] = gacc[0];
+    } else {
+      for (int e = threadIdx.x, i = 0; e < nd * nd; e += blockDim.x, ++i)
+        out[2 * kAlphas + nd + e] = gacc[NDT <= 8 ? 0 : i];
+    }
   }
 }
 
@@ -703,22 +759,38 @@ __device__ void newton_body(const double* __restrict__ R, const double* __restri
     K[n * (N + 1) + N] = 0.0;
   }
   __syncthreads();
-  // Gaussian elimination with partial pivoting (single thread picks the
-  // pivot, all threads eliminate).
+  // Gaussian elimination with partial pivoting: warp 0 picks the pivot (the
+  // first row holding the largest |entry|, as a sequential scan would), the
+  // multipliers are formed once per row, all threads eliminate.
   __shared__ int piv;
   __shared__ int singular;
+  __shared__ double mult[kMaxCols + 1];
+  __shared__ double xs[kMaxCols + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) singular = 0;
   for (int col = 0; col < N; ++col) {
-    if (threadIdx.x == 0) {
-      int p = col;
-      double best = fabs(K[col * (N + 1) + col]);
-      for (int r = col + 1; r < N; ++r)
-        if (fabs(K[r * (N + 1) + col]) > best) {
-          best = fabs(K[r * (N + 1) + col]);
+    if (warp == 0) {
+      int p = N;
+      double best = -1.0;
+      for (int r = col + lane; r < N; r += 32) {
+        const double v = fabs(K[r * (N + 1) + col]);
+        if (v > best) {
+          best = v;
           p = r;
         }
-      piv = p;
-      if (best == 0.0) singular = 1;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int op = __shfl_xor_sync(0xffffffffu, p, o);
+        if (ob > best || (ob == best && op < p)) {
+          best = ob;
+          p = op;
+        }
+      }
+      if (lane == 0) {
+        piv = p;
+        if (best == 0.0) singular = 1;
+      }
     }
     __syncthreads();
     if (piv != col)
@@ -729,20 +801,27 @@ __device__ void newton_body(const double* __restrict__ R, const double* __restri
       }
     __syncthreads();
     const double d = K[col * (N + 1) + col];
+    for (int r = col + 1 + (int)threadIdx.x; r < N; r += blockDim.x) mult[r] = K[r * (N + 1) + col] / d;
+    __syncthreads();
     for (int e = threadIdx.x; e < (N - col - 1) * (N - col); e += blockDim.x) {
       const int r = col + 1 + e / (N - col), j = col + 1 + e % (N - col);
-      const double f = K[r * (N + 1) + col] / d;
-      K[r * (N + 1) + j] -= f * K[col * (N + 1) + j];
+      K[r * (N + 1) + j] -= mult[r] * K[col * (N + 1) + j];
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    double x[kMaxCols + 1];
+  // Back substitution, one warp (lane-split dot products).
+  if (warp == 0) {
     for (int r = N - 1; r >= 0; --r) {
-      double t = K[r * (N + 1) + N];
-      for (int j = r + 1; j < N; ++j) t -= K[r * (N + 1) + j] * x[j];
-      x[r] = t / K[r * (N + 1) + r];
+      double t = 0.0;
+      for (int j = r + 1 + lane; j < N; j += 32) t = fma(K[r * (N + 1) + j], xs[j], t);
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) xs[r] = (K[r * (N + 1) + N] - t) / K[r * (N + 1) + r];
+      __syncwarp();
     }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double* x = xs;
     bool finite = !singular;
     double dec = 0.0;
     for (int k = 0; k < n; ++k) {
@@ -981,8 +1060,8 @@ struct DevBuf {
       return fset_err(err, errlen, RPG_E_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
   } while (0)
 
-size_t tsqr_smem(int n_vars) {
-  return sizeof(double) * ((size_t)kMaxCols * kMaxCols + (size_t)kTile * kMaxCols + 32 + kMaxCols) +
+size_t tsqr_smem(int ncols) {
+  return sizeof(double) * ((size_t)ncols * ncols + (size_t)kTile * ncols + 32 + kMaxCols) +
          (size_t)kMaxCols * RPG_MAX_VARS + 16;
 }
 
@@ -990,32 +1069,32 @@ size_t tsqr_smem(int n_vars) {
 int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, char* err,
          size_t errlen) {
   const int64_t tiles = (F.m + kTile - 1) / kTile;
-  int G = (int)std::min<int64_t>(tiles, 2LL * sms);
+  int G = (int)std::min<int64_t>(tiles, 4LL * sms);
   if (G < 1) G = 1;
   FCUDA(cudaMalloc(&Rbuf->p, sizeof(double) * (size_t)G * ncols * ncols));
-  const size_t sm1 = tsqr_smem(F.n_vars);
+  const size_t sm1 = tsqr_smem(ncols);
   FCUDA(cudaFuncSetAttribute(tsqr_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
   tsqr_tiles<<<G, kFitThreads, sm1, s>>>(F, Rbuf->as<double>());
   FCUDA(cudaGetLastError());
-  const size_t sm2 = sizeof(double) * (2 * (size_t)kMaxCols * kMaxCols + 32 + kMaxCols);
+  const size_t sm2 = sizeof(double) * (2 * (size_t)ncols * ncols + 32 + kMaxCols);
   FCUDA(cudaFuncSetAttribute(tsqr_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-  // Tree over the G factors: at every level slot 2b absorbs slot 2b+1; then
-  // survivors are compacted by re-striding (slot 2b -> b) with a copy.
+  // Tree over the G factors, one launch per level, ping-ponging between
+  // Rbuf and tmp; the root ends in Rbuf.
   int count = G;
   DevBuf tmp;
   FCUDA(cudaMalloc(&tmp.p, sizeof(double) * (size_t)G * ncols * ncols));
+  double* in = Rbuf->as<double>();
+  double* outb = tmp.as<double>();
   while (count > 1) {
-    tsqr_combine<<<count / 2, kFitThreads, sm2, s>>>(Rbuf->as<double>(), count, ncols);
-    FCUDA(cudaGetLastError());
     const int next = (count + 1) / 2;
-    for (int b = 0; b < next; ++b)
-      FCUDA(cudaMemcpyAsync(tmp.as<double>() + (size_t)b * ncols * ncols,
-                            Rbuf->as<double>() + (size_t)(2 * b) * ncols * ncols,
-                            sizeof(double) * ncols * ncols, cudaMemcpyDeviceToDevice, s));
-    FCUDA(cudaMemcpyAsync(Rbuf->p, tmp.p, sizeof(double) * (size_t)next * ncols * ncols,
-                          cudaMemcpyDeviceToDevice, s));
+    tsqr_combine<<<next, kFitThreads, sm2, s>>>(in, count, ncols, outb);
+    FCUDA(cudaGetLastError());
+    std::swap(in, outb);
     count = next;
   }
+  if (in != Rbuf->as<double>())
+    FCUDA(cudaMemcpyAsync(Rbuf->p, in, sizeof(double) * (size_t)ncols * ncols,
+                          cudaMemcpyDeviceToDevice, s));
   return RPG_OK;
 }
 
@@ -1032,15 +1111,21 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
   const int W = 2 * kAlphas + F.nd + F.nd * F.nd;
   if (!P->part.p) {
     const int64_t tiles = (F.m + kPassRows - 1) / kPassRows;
-    P->G = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2LL * sms));
+    P->G = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 4LL * sms));
     P->nd = F.nd;
     FCUDA(cudaMalloc(&P->part.p, sizeof(double) * (size_t)P->G * W));
     FCUDA(cudaMalloc(&P->out.p, sizeof(double) * W));
   }
-  const size_t sm = sizeof(double) * ((size_t)kPassRows * kMaxCols + 32 + kAlphas * kMaxCols) +
-                    (size_t)kMaxCols * RPG_MAX_VARS + 16;
-  FCUDA(cudaFuncSetAttribute(den_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  den_pass<<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>(), src);
+  const size_t sm = sizeof(double) * ((size_t)kPassRows * F.nd + 32 + kAlphas * F.nd) +
+                    (size_t)F.nd * RPG_MAX_VARS + 16;
+  if (F.nd <= 8) {
+    FCUDA(cudaFuncSetAttribute(den_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    den_pass<8><<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>(), src);
+  } else {
+    FCUDA(cudaFuncSetAttribute(den_pass<kMaxCols>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    den_pass<kMaxCols><<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton,
+                                                     P->part.as<double>(), src);
+  }
   FCUDA(cudaGetLastError());
   den_pass_final<<<1, 256, 0, s>>>(P->part.as<double>(), P->G, F.nd, P->out.as<double>(), src.ctl);
   return RPG_OK;
