@@ -487,10 +487,11 @@ struct CtlSrc {
 // NDT: compile-time bound on nd (8 = the default (1,1,1) denominator basis)
 // so the per-row monomials and accumulators stay in registers.
 template <int NDT>
-__global__ void __launch_bounds__(kFitThreads)
-den_pass(const FitParams F, const double* __restrict__ cd, const double* __restrict__ dd,
-         const double* __restrict__ alphas, int n_alpha, int newton,
-         double* __restrict__ partial /* per block: 2*kAlphas + nd + nd*nd */, CtlSrc src) {
+__device__ __forceinline__ void den_pass_body(const FitParams& F, const double* __restrict__ cd,
+                                              const double* __restrict__ dd,
+                                              const double* __restrict__ alphas, int n_alpha,
+                                              int newton, double* __restrict__ partial,
+                                              const CtlSrc& src) {
   extern __shared__ __align__(16) double fsm[];
   const int nd = F.nd;
   if (src.ctl) {
@@ -648,9 +649,16 @@ den_pass(const FitParams F, const double* __restrict__ cd, const double* __restr
 }
 
 // Sums the per-block partials of den_pass (min for the q minima).
-__global__ void den_pass_final(const double* __restrict__ partial, int G, int nd,
-                               double* __restrict__ out, const MinCtl* __restrict__ ctl) {
-  if (ctl && ctl->phase >= kMinDone) return;
+template <int NDT>
+__global__ void __launch_bounds__(kFitThreads)
+den_pass(const FitParams F, const double* __restrict__ cd, const double* __restrict__ dd,
+         const double* __restrict__ alphas, int n_alpha, int newton,
+         double* __restrict__ partial /* per block: 2*kAlphas + nd + nd*nd */, CtlSrc src) {
+  den_pass_body<NDT>(F, cd, dd, alphas, n_alpha, newton, partial, src);
+}
+
+__device__ __forceinline__ void den_pass_reduce(const double* __restrict__ partial, int G, int nd,
+                                                double* __restrict__ out) {
   const int W = 2 * kAlphas + nd + nd * nd;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int e = warp; e < W; e += nw) {
@@ -663,6 +671,12 @@ __global__ void den_pass_final(const double* __restrict__ partial, int G, int nd
     }
     if (lane == 0) out[e] = t;
   }
+}
+
+__global__ void den_pass_final(const double* __restrict__ partial, int G, int nd,
+                               double* __restrict__ out, const MinCtl* __restrict__ ctl) {
+  if (ctl && ctl->phase >= kMinDone) return;
+  den_pass_reduce(partial, G, nd, out);
 }
 
 // ||R S v||^2 for the n x n upper-triangular R (row-major) and scale S.
@@ -854,11 +868,12 @@ __device__ __forceinline__ void ctl_end_inner(MinCtl* ctl) {
 //           accept the first (in halving order) with q > 0 and Armijo
 //           decrease, else continue halving (the inner loop ends when alpha
 //           drops to 1e-18) — polyfit.hpp:279-306.
-__global__ void __launch_bounds__(kFitThreads)
-ctl_step(const double* __restrict__ R, const double* __restrict__ S,
-         const double* __restrict__ gsum, const double* __restrict__ pass_out,
-         double* __restrict__ c, int nn, int nd, double* __restrict__ dc,
-         MinCtl* __restrict__ ctl, MinState* __restrict__ scratch) {
+__device__ __forceinline__ void ctl_step_body(const double* __restrict__ R, const double* __restrict__ S,
+                                              const double* __restrict__ gsum,
+                                              const double* __restrict__ pass_out,
+                                              double* __restrict__ c, int nn, int nd,
+                                              double* __restrict__ dc, MinCtl* __restrict__ ctl,
+                                              MinState* __restrict__ scratch) {
   const int ph = ctl->phase;
   if (ph >= kMinDone) return;
   const int n = nn + nd;
@@ -887,16 +902,23 @@ ctl_step(const double* __restrict__ R, const double* __restrict__ S,
   __shared__ int accepted;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int na = ctl->n_alpha;
+  __shared__ double rows[kAlphas][kMaxCols];
   if (warp < na) {
+    // ||R S cn||^2 with the row sums in parallel and the sum of squares in
+    // row order — the operation order of phi0 (newton_body), so a step of
+    // vanishing length reproduces phi0 exactly.
     const double al = ctl->al[warp];
-    double acc = 0.0;
     for (int i = lane; i < n; i += 32) {
       double t = 0.0;
       for (int k = i; k < n; ++k) t = fma(R[i * n + k], S[k] * (c[k] + al * dc[k]), t);
-      acc = fma(t, t, acc);
+      rows[warp][i] = t;
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) phis[warp] = acc - ctl->mu * pass_out[2 * warp + 1];
+    __syncwarp();
+    if (lane == 0) {
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) acc = fma(rows[warp][i], rows[warp][i], acc);
+      phis[warp] = acc - ctl->mu * pass_out[2 * warp + 1];
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -928,6 +950,31 @@ ctl_step(const double* __restrict__ R, const double* __restrict__ S,
       ctl->alpha = next;
     }
   }
+}
+
+// One whole minimizer step in one launch: every CTA runs its share of the
+// controlled sample pass; the last CTA to finish (threadfence + counter)
+// reduces the partials and applies the Newton / line-search update, then
+// re-arms the counter.  No-op for every CTA once the loop is done.
+template <int NDT>
+__global__ void __launch_bounds__(kFitThreads)
+min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __restrict__ pass_out,
+         unsigned* __restrict__ counter, const double* __restrict__ R, const double* __restrict__ S,
+         const double* __restrict__ gsum, double* __restrict__ c, double* __restrict__ dc,
+         MinCtl* __restrict__ ctl, MinState* __restrict__ scratch) {
+  if (src.ctl->phase >= kMinDone) return;
+  den_pass_body<NDT>(F, nullptr, nullptr, nullptr, 1, 1, partial, src);
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  den_pass_reduce(partial, gridDim.x, F.nd, pass_out);
+  __syncthreads();
+  ctl_step_body(R, S, gsum, pass_out, c, F.nn, F.nd, dc, ctl, scratch);
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 __global__ void to_raw(const double* __restrict__ c, const double* __restrict__ S, int n,
@@ -1100,6 +1147,11 @@ int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, c
 
 }  // namespace
 
+size_t den_pass_smem(const FitParams& F) {
+  return sizeof(double) * ((size_t)kPassRows * F.nd + 32 + kAlphas * F.nd) +
+         (size_t)F.nd * RPG_MAX_VARS + 16;
+}
+
 struct Pass {
   DevBuf part, out;
   int G = 0, nd = 0;
@@ -1116,8 +1168,7 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
     FCUDA(cudaMalloc(&P->part.p, sizeof(double) * (size_t)P->G * W));
     FCUDA(cudaMalloc(&P->out.p, sizeof(double) * W));
   }
-  const size_t sm = sizeof(double) * ((size_t)kPassRows * F.nd + 32 + kAlphas * F.nd) +
-                    (size_t)F.nd * RPG_MAX_VARS + 16;
+  const size_t sm = den_pass_smem(F);
   if (F.nd <= 8) {
     FCUDA(cudaFuncSetAttribute(den_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     den_pass<8><<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>(), src);
@@ -1158,7 +1209,6 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   FCUDA(cudaStreamSynchronize(s));
   if (!hs.ok) return RPG_OK;
   const size_t smk = sizeof(double) * ((size_t)(kMaxCols + 1) * (kMaxCols + 2) + 3 * kMaxCols);
-  FCUDA(cudaFuncSetAttribute(ctl_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smk));
   DevBuf ctlb;
   FCUDA(cudaMalloc(&ctlb.p, sizeof(MinCtl)));
   MinCtl hc{};
@@ -1167,6 +1217,13 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   hc.n_alpha = 1;
   FCUDA(cudaMemcpyAsync(ctlb.p, &hc, sizeof(hc), cudaMemcpyHostToDevice, s));
   MinCtl* dctl = ctlb.as<MinCtl>();
+  DevBuf counter;
+  FCUDA(cudaMalloc(&counter.p, sizeof(unsigned)));
+  FCUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), s));
+  const size_t smstep = std::max(smk, den_pass_smem(F));
+  FCUDA(cudaFuncSetAttribute(min_step<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smstep));
+  FCUDA(cudaFuncSetAttribute(min_step<kMaxCols>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smstep));
   const CtlSrc src{dctl, c.as<double>(), dc.as<double>(), S};
   // Steps (controlled den_pass + reduction + Newton-or-line update) are
   // enqueued in chunks; the host only polls the phase between chunks.
@@ -1174,15 +1231,22 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   constexpr int kChunk = 24;
   for (int done = 0, steps = 0; !done && steps < 16 * 40 * 16; steps += kChunk) {
     for (int i = 0; i < kChunk; ++i) {
-      rc = run_den_pass(F, nullptr, nullptr, nullptr, 1, 1, sms, &P, s, err, errlen, src);
-      if (rc) return rc;
-      ctl_step<<<1, kFitThreads, smk, s>>>(R, S, gsum, P.out.as<double>(), c.as<double>(), nn, nd,
-                                           dc.as<double>(), dctl, st.as<MinState>());
+      if (F.nd <= 8)
+        min_step<8><<<P.G, kFitThreads, smstep, s>>>(F, src, P.part.as<double>(), P.out.as<double>(),
+                                                     counter.as<unsigned>(), R, S, gsum, c.as<double>(),
+                                                     dc.as<double>(), dctl, st.as<MinState>());
+      else
+        min_step<kMaxCols><<<P.G, kFitThreads, smstep, s>>>(
+            F, src, P.part.as<double>(), P.out.as<double>(), counter.as<unsigned>(), R, S, gsum,
+            c.as<double>(), dc.as<double>(), dctl, st.as<MinState>());
     }
     FCUDA(cudaGetLastError());
     FCUDA(cudaMemcpyAsync(&hc, ctlb.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     FCUDA(cudaStreamSynchronize(s));
     done = hc.phase >= kMinDone;
+    if (done && getenv("RPG_FIT_TRACE"))
+      fprintf(stderr, "[rpg_fit] minimizer: <= %d steps, phase %d, outer %d, inner %d\n",
+              steps + kChunk, hc.phase, hc.outer, hc.inner);
   }
   if (hc.phase == kMinFail) return RPG_OK;
   to_raw<<<1, 32, 0, s>>>(c.as<double>(), S, n, out_raw, fin.as<int>());
