@@ -1163,7 +1163,14 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
   const int W = 2 * kAlphas + F.nd + F.nd * F.nd;
   if (!P->part.p) {
     const int64_t tiles = (F.m + kPassRows - 1) / kPassRows;
-    P->G = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 4LL * sms));
+    // CTAs per SM of the sample passes (RPG_FIT_PASS_CTAS overrides: more
+    // CTAs hide the pass's latency, fewer shorten the serial partial
+    // reduction of the fused minimizer step).
+    static const int per_sm = [] {
+      const char* e = getenv("RPG_FIT_PASS_CTAS");
+      return e ? std::max(1, atoi(e)) : 4;
+    }();
+    P->G = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)per_sm * sms));
     P->nd = F.nd;
     FCUDA(cudaMalloc(&P->part.p, sizeof(double) * (size_t)P->G * W));
     FCUDA(cudaMalloc(&P->out.p, sizeof(double) * W));
