@@ -15,6 +15,13 @@
 //   pipe::SearchOptions / SearchRow / SearchResult /
 //   search_optimal                                        pipeline.hpp:438-680
 //   pipe::format_search_{csv,text,jsonl}                  pipeline.hpp:897-934
+//   poly::PointValueSet / fit_rational                    polyfit.hpp:133-135, 337-427
+//   data::Sample / SampleSet, pipe::sample_variables /
+//   default_bounds / metric_points / fit_all_metrics      datakit.hpp:40-75, pipeline.hpp:72-184
+//   perf::KernelMetrics / MwpCwpBreakdown /
+//   active_blocks / active_warps / occupancy /
+//   mwpcwp_cycles                                          perfmodel.hpp:68-77, 239-395
+//   poly::from_altarr / ratfunc_from_altarr (KLARAPTOR AltArr_t interop)
 // A caller of the reference's `--models` search path (ratprog_cli.cpp:
 // 277-332) compiles against this header unchanged: `generate_rp` returns an
 // ir::RationalProgram that carries the metric spec, and `search_optimal`
@@ -125,6 +132,67 @@ inline RationalFunction ratfunc_from_altarr(const rpg_altarr& num, const rpg_alt
   return RationalFunction{from_altarr(num, variables), from_altarr(den, variables)};
 }
 
+// ---- the fit (polyfit.hpp:133-135, 337-427) on the GPU (rpg_fit_rational)
+struct DegenerateFit : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct SvdFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline constexpr double kDefaultRankTol = 1e-10;
+
+struct PointValueSet {
+  std::vector<std::vector<double>> points;
+  std::vector<double> values;
+};
+
+// poly::fit_rational: homogeneous least-squares rational fit over the
+// graded-lex bases of `bounds`, including the positivity safeguard.  Every
+// FLOP runs in the K3 kernels; this only packs arguments.
+inline std::pair<RationalFunction, FitReport> fit_rational(const PointValueSet& pv,
+                                                           const std::vector<std::string>& variables,
+                                                           const DegreeBounds& bounds,
+                                                           double rank_tol = kDefaultRankTol,
+                                                           int device = 0) {
+  const size_t nv = variables.size();
+  if (bounds.num.size() != nv || bounds.den.size() != nv)
+    throw DimensionMismatch("fit_rational: degree bounds do not match the variables");
+  if (pv.points.size() != pv.values.size())
+    throw DimensionMismatch("fit_rational: points/values size mismatch");
+  std::vector<double> X;
+  X.reserve(pv.points.size() * nv);
+  for (const auto& x : pv.points) {
+    if (x.size() != nv) throw DimensionMismatch("fit_rational: point dimension mismatch");
+    X.insert(X.end(), x.begin(), x.end());
+  }
+  const auto nb = monomial_basis(bounds.num), db = monomial_basis(bounds.den);
+  const size_t n = nb.size() + db.size();
+  std::vector<double> coef(n), sigma(std::max<size_t>(1, std::min(pv.values.size(), n)));
+  int32_t rank = 0, truncated = 0, safeguard = 0;
+  double residual = 0.0;
+  char err[512] = {0};
+  const int rc = rpg_fit_rational(X.data(), pv.values.data(), (int64_t)pv.values.size(),
+                                  (int32_t)nv, bounds.num.data(), bounds.den.data(), rank_tol,
+                                  device, coef.data(), sigma.data(), &rank, &truncated, &residual,
+                                  &safeguard, err, sizeof err);
+  if (rc == RPG_E_FIT) {
+    if (std::string(err).find("svd") == 0) throw SvdFailure(err);
+    throw DegenerateFit(err);
+  }
+  if (rc == RPG_E_INVALID) throw std::invalid_argument(err);
+  if (rc != RPG_OK) throw std::runtime_error(std::string("librpgpu: ") + err);
+  RationalFunction f;
+  f.num = Polynomial{variables, nb, std::vector<double>(coef.begin(), coef.begin() + nb.size())};
+  f.den = Polynomial{variables, db, std::vector<double>(coef.begin() + nb.size(), coef.end())};
+  FitReport rep;
+  rep.residual_norm = residual;
+  rep.numerical_rank = rank;
+  rep.singular_values.assign(sigma.begin(), sigma.begin() + std::min(pv.values.size(), n));
+  rep.truncated = truncated != 0;
+  return {std::move(f), std::move(rep)};
+}
+
 }  // namespace poly
 
 // ---------------------------------------------------------------------------
@@ -142,6 +210,22 @@ struct DeviceProfile {
   double freq_GHz = 0, mem_latency_cycles = 0, departure_del_coal_cycles = 0,
          departure_del_uncoal_cycles = 0, mem_bandwidth_GBps = 0, issue_cycles = 0;
   long long load_bytes_per_warp = 0, uncoal_per_mw = 0;
+};
+
+struct ZeroOccupancy : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// perf::KernelMetrics (perfmodel.hpp:68-77).
+struct KernelMetrics {
+  double regs_per_thread = 0;
+  double shared_words_per_block = 0;
+  double comp_insts_per_thread = 0;
+  double mem_insts_per_thread = 0;
+  double uncoal_mem_insts_per_thread = 0;
+  double coal_mem_insts_per_thread = 0;
+  double synch_insts_per_block = 0;
+  double total_blocks = 0;
 };
 
 struct LaunchConfig {
@@ -165,6 +249,107 @@ inline const char* case_name(CaseTag t) {
     case CaseTag::MwpBound: return "mwp_bound";
   }
   return "?";
+}
+
+// perf::MwpCwpBreakdown (perfmodel.hpp:284-296).  The GPU direct-model kernel
+// exports b_active, N, the case and the total; the intermediate terms are
+// not exported and stay NaN.
+struct MwpCwpBreakdown {
+  long long b_active = 0;
+  long long n_active_warps = 0;
+  double mem_cycles = NAN;
+  double comp_cycles = NAN;
+  double mwp = NAN;
+  double cwp = NAN;
+  double rep = NAN;
+  CaseTag case_tag = CaseTag::CwpBound;
+  double cycles_pre_synch = NAN;
+  double synch_cost = NAN;
+  double total_cycles = 0;
+};
+
+namespace detail {
+inline rpg_profile profile_to_rpg(const DeviceProfile& hw) {
+  rpg_profile p;
+  p.R_max = hw.R_max; p.Z_max = hw.Z_max; p.T_max = hw.T_max; p.B_max = hw.B_max;
+  p.W_max = hw.W_max; p.num_SM = hw.num_SM; p.freq_GHz = hw.freq_GHz;
+  p.mem_latency_cycles = hw.mem_latency_cycles;
+  p.departure_del_coal_cycles = hw.departure_del_coal_cycles;
+  p.departure_del_uncoal_cycles = hw.departure_del_uncoal_cycles;
+  p.mem_bandwidth_GBps = hw.mem_bandwidth_GBps; p.issue_cycles = hw.issue_cycles;
+  p.load_bytes_per_warp = hw.load_bytes_per_warp; p.uncoal_per_mw = hw.uncoal_per_mw;
+  return p;
+}
+
+// One row through rpg_mwpcwp_cycles_batch (the GPU direct model).
+inline void direct_row(const DeviceProfile& hw, const KernelMetrics& m, const LaunchConfig& c,
+                       RepMode mode, double* total, int32_t* b, int32_t* w, uint8_t* tag,
+                       int32_t* status) {
+  const double mv[RPG_N_METRICS] = {m.regs_per_thread, m.shared_words_per_block,
+                                    m.comp_insts_per_thread, m.uncoal_mem_insts_per_thread,
+                                    m.coal_mem_insts_per_thread, m.synch_insts_per_block,
+                                    m.total_blocks};
+  const rpg_profile p = profile_to_rpg(hw);
+  const rpg_config cfg{c.bx, c.by, c.bz};
+  char err[512] = {0};
+  const int rc = rpg_mwpcwp_cycles_batch(&p, mv, &cfg, 1,
+                                         mode == RepMode::Ceil ? RPG_REP_CEIL : RPG_REP_REAL, 0,
+                                         total, b, w, tag, status, err, sizeof err);
+  if (rc == RPG_E_PROFILE) throw ProfileError(err);
+  if (rc == RPG_E_INVALID) throw std::invalid_argument(err);
+  if (rc != RPG_OK) throw std::runtime_error(std::string("librpgpu: ") + err);
+}
+}  // namespace detail
+
+// perf::active_blocks / active_warps / occupancy (perfmodel.hpp:239-266),
+// evaluated by the GPU direct-model kernel.
+inline long long active_blocks(const DeviceProfile& hw, double R, double Z, long long T) {
+  KernelMetrics m;
+  m.regs_per_thread = R;
+  m.shared_words_per_block = Z;
+  int32_t b = 0, w = 0, st = 0;
+  uint8_t tag = 0;
+  double tot = 0;
+  detail::direct_row(hw, m, LaunchConfig{T, 1, 1}, RepMode::Real, &tot, &b, &w, &tag, &st);
+  return b;
+}
+
+inline long long active_warps(const DeviceProfile& hw, long long b_active, long long T) {
+  if (b_active <= 0) return 0;
+  const long long w = b_active * T / 32;  // floor, perfmodel.hpp:258
+  return w < hw.W_max ? w : hw.W_max;
+}
+
+inline double occupancy(const DeviceProfile& hw, double R, double Z, long long T) {
+  if (hw.W_max <= 0) return 0.0;
+  return static_cast<double>(active_warps(hw, active_blocks(hw, R, Z, T), T)) /
+         static_cast<double>(hw.W_max);
+}
+
+// perf::mwpcwp_cycles (perfmodel.hpp:298-395) on the GPU.  Same exceptions:
+// ModelError for negative or inconsistent metrics, ZeroOccupancy when no
+// block fits.
+inline MwpCwpBreakdown mwpcwp_cycles(const DeviceProfile& hw, const KernelMetrics& m,
+                                     const LaunchConfig& config, RepMode mode = RepMode::Real) {
+  const double sum = m.uncoal_mem_insts_per_thread + m.coal_mem_insts_per_thread;
+  if (std::fabs(sum - m.mem_insts_per_thread) > 1e-9 * std::max(1.0, m.mem_insts_per_thread))
+    throw ModelError("metrics inconsistent: uncoal + coal must equal mem_insts");
+  int32_t b = 0, w = 0, st = 0;
+  uint8_t tag = 0;
+  double tot = 0;
+  detail::direct_row(hw, m, config, mode, &tot, &b, &w, &tag, &st);
+  if (st == 2 || st == 3 || m.mem_insts_per_thread < 0) throw ModelError("metrics must be non-negative");
+  if (st == 1)
+    throw ZeroOccupancy(b == 0 ? "configuration cannot launch (no resident block)"
+                               : "configuration yields no resident warp");
+  MwpCwpBreakdown r;
+  r.b_active = b;
+  r.n_active_warps = w;
+  r.case_tag = tag == RPG_CASE_BOTH_SATURATED ? CaseTag::BothSaturated
+               : tag == RPG_CASE_MWP_BOUND   ? CaseTag::MwpBound
+                                             : CaseTag::CwpBound;
+  r.total_cycles = tot;
+  return r;
 }
 
 namespace detail {
@@ -312,6 +497,27 @@ struct EmitOptions {
 
 // ---------------------------------------------------------------------------
 namespace data {
+
+// data::Sample / SampleSet (datakit.hpp:40-75): the fit's input rows.
+struct Provenance {
+  enum class Kind { Measured, Synthetic };
+  Kind kind = Kind::Measured;
+  std::uint64_t seed = 0;
+  double noise_rel = 0;
+};
+
+struct Sample {
+  std::vector<long long> data_params;
+  perf::LaunchConfig config;
+  std::map<std::string, double> metric_values;
+};
+
+struct SampleSet {
+  std::vector<std::string> metric_names;
+  std::vector<Sample> samples;
+  Provenance provenance;
+  std::size_t dims() const { return samples.empty() ? 0 : samples.front().data_params.size(); }
+};
 
 // data::enumerate_configs (datakit.hpp:79-94).
 inline std::vector<perf::LaunchConfig> enumerate_configs(long long max_threads = 1024,
@@ -484,6 +690,99 @@ struct MetricModelSet {
   std::map<std::string, double> constants;
   std::map<std::string, std::string> failures;
 };
+
+struct AllMetricsFailed : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// pipe::sample_variables / default_bounds / metric_points (pipeline.hpp:72-133).
+inline std::vector<std::string> sample_variables(const data::SampleSet& set) {
+  std::vector<std::string> vars;
+  for (std::size_t i = 1; i <= set.dims(); ++i) vars.push_back("D" + std::to_string(i));
+  vars.push_back("bx");
+  vars.push_back("by");
+  for (const data::Sample& s : set.samples)
+    if (s.config.bz != 1) {
+      vars.push_back("bz");
+      break;
+    }
+  return vars;
+}
+
+inline poly::DegreeBounds default_bounds(std::size_t n_variables) {
+  poly::DegreeBounds b;
+  b.num.assign(n_variables, 2);
+  b.den.assign(n_variables, 1);
+  return b;
+}
+
+inline poly::PointValueSet metric_points(const data::SampleSet& set, const std::string& metric,
+                                         const std::vector<std::string>& variables) {
+  poly::PointValueSet out;
+  out.points.reserve(set.samples.size());
+  out.values.reserve(set.samples.size());
+  for (const data::Sample& s : set.samples) {
+    auto it = s.metric_values.find(metric);
+    if (it == s.metric_values.end())
+      throw PipelineError("sample set has no metric column '" + metric + "'");
+    std::vector<double> x;
+    x.reserve(variables.size());
+    for (const std::string& v : variables) {
+      if (v == "bx") x.push_back((double)s.config.bx);
+      else if (v == "by") x.push_back((double)s.config.by);
+      else if (v == "bz") x.push_back((double)s.config.bz);
+      else {
+        const std::size_t k = std::stoul(v.substr(1));
+        if (k < 1 || k > s.data_params.size())
+          throw PipelineError("variable '" + v + "' exceeds the sample's data-parameter count");
+        x.push_back((double)s.data_params[k - 1]);
+      }
+    }
+    out.points.push_back(std::move(x));
+    out.values.push_back(it->second);
+  }
+  return out;
+}
+
+struct FitOptions {
+  double rank_tol = poly::kDefaultRankTol;
+};
+
+// pipe::fit_all_metrics (pipeline.hpp:145-184): one GPU rational fit per
+// metric column; numerical failures are recorded per metric, a full wipeout
+// raises AllMetricsFailed.
+inline MetricModelSet fit_all_metrics(const data::SampleSet& samples,
+                                      const std::map<std::string, poly::DegreeBounds>& bounds,
+                                      const std::map<std::string, double>& constants,
+                                      const FitOptions& opts = {}) {
+  if (samples.samples.empty()) throw std::invalid_argument("fit_all_metrics: sample set is empty");
+  MetricModelSet out;
+  out.variables = sample_variables(samples);
+  out.constants = constants;
+  for (const std::string& metric : samples.metric_names) {
+    if (constants.count(metric))
+      throw PipelineError("metric '" + metric + "' is both a sample column and a declared constant");
+    poly::DegreeBounds b = bounds.count(metric) ? bounds.at(metric) : default_bounds(out.variables.size());
+    if (b.num.size() != out.variables.size() || b.den.size() != out.variables.size())
+      throw PipelineError("degree bounds for metric '" + metric + "' must have " +
+                          std::to_string(out.variables.size()) + " entries per side");
+    try {
+      auto pv = metric_points(samples, metric, out.variables);
+      auto fitted = poly::fit_rational(pv, out.variables, b, opts.rank_tol);
+      out.models[metric] = MetricModel{std::move(fitted.first), std::move(fitted.second)};
+    } catch (const poly::DegenerateFit& e) {
+      out.failures[metric] = e.what();
+    } catch (const poly::SvdFailure& e) {
+      out.failures[metric] = e.what();
+    }
+  }
+  if (out.models.empty()) {
+    std::string msg = "no metric could be fitted:";
+    for (const auto& f : out.failures) msg += " [" + f.first + ": " + f.second + "]";
+    throw AllMetricsFailed(msg);
+  }
+  return out;
+}
 
 namespace detail {
 

@@ -152,6 +152,81 @@ static void gpu_tests() {
   s2.variables = {"D2", "bx", "by"};
   for (auto& kv : s2.models) kv.second.num.variables = kv.second.den.variables = s2.variables;
   CHECK(throws_with<pipe::PipelineError>([&] { pipe::search_optimal(s2, {64}, sample, space); }, "D2"));
+
+  // Direct model on the GPU: the reference's known answers
+  // (test_perfmodel.cpp:228-290, 373-377).
+  perf::DeviceProfile sh = perf::load_profile(root + "/data/sample_device.profile");
+  CHECK(perf::active_blocks(sh, 20, 0, 256) == 6);
+  CHECK(perf::active_warps(sh, 6, 256) == 48);
+  CHECK(perf::occupancy(sh, 20, 0, 256) == 1.0);
+  CHECK(perf::active_blocks(sh, 64, 0, 256) == 4);
+  CHECK(perf::active_blocks(sh, 0, 5000, 256) == 2);
+  CHECK(perf::active_blocks(sh, 20, 0, 2048) == 0);
+  CHECK(perf::active_blocks(sh, 300, 0, 1024) == 0);
+  perf::DeviceProfile oh;
+  oh.R_max = 100000; oh.Z_max = 100000; oh.T_max = 1024; oh.B_max = 4; oh.W_max = 48; oh.num_SM = 1;
+  oh.freq_GHz = 1; oh.mem_latency_cycles = 300; oh.departure_del_coal_cycles = 150;
+  oh.departure_del_uncoal_cycles = 50; oh.mem_bandwidth_GBps = 2; oh.issue_cycles = 4;
+  oh.load_bytes_per_warp = 100; oh.uncoal_per_mw = 5;
+  perf::KernelMetrics km;
+  km.comp_insts_per_thread = 18; km.uncoal_mem_insts_per_thread = 1; km.coal_mem_insts_per_thread = 1;
+  km.mem_insts_per_thread = 2; km.synch_insts_per_block = 0; km.total_blocks = 4;
+  auto br = perf::mwpcwp_cycles(oh, km, perf::LaunchConfig{32, 1, 1});
+  CHECK(br.b_active == 4 && br.n_active_warps == 4);
+  CHECK(br.case_tag == perf::CaseTag::CwpBound && br.total_cycles == 1640.0);
+  perf::KernelMetrics bad = km;
+  bad.mem_insts_per_thread = 3;
+  CHECK(throws_with<perf::ModelError>([&] { perf::mwpcwp_cycles(oh, bad, perf::LaunchConfig{32, 1, 1}); },
+                                      "metrics inconsistent"));
+  perf::DeviceProfile oh1 = oh;
+  oh1.B_max = 1;
+  CHECK(throws_with<perf::ZeroOccupancy>([&] { perf::mwpcwp_cycles(oh1, km, perf::LaunchConfig{8, 1, 1}); },
+                                         "no resident"));
+
+  // The fit on the GPU: an exact rational ground truth is recovered
+  // (test_polyfit.cpp:142-228 criterion: coefficients up to scale, < 1e-8).
+  poly::PointValueSet pv;
+  for (int d = 64; d <= 4096; d += 64)
+    for (int bx : {1, 2, 4, 8, 16, 32})
+      for (int by : {1, 2, 4, 8}) {
+        pv.points.push_back({(double)d, (double)bx, (double)by});
+        pv.values.push_back((3.0 * d + 20.0 * bx) / (1.0 + 0.5 * by));
+      }
+  poly::DegreeBounds fb{{1, 1, 0}, {0, 0, 1}};
+  auto fitted = poly::fit_rational(pv, {"D1", "bx", "by"}, fb);
+  const auto& fn = fitted.first;
+  double worst = 0;
+  for (size_t i = 0; i < pv.points.size(); i += 7) {
+    double p = 0, q = 0;
+    for (size_t k = 0; k < fn.num.coeffs.size(); ++k) {
+      double m = 1;
+      for (int v = 0; v < 3; ++v) m *= std::pow(pv.points[i][v], fn.num.basis[k][v]);
+      p += fn.num.coeffs[k] * m;
+    }
+    for (size_t k = 0; k < fn.den.coeffs.size(); ++k) {
+      double m = 1;
+      for (int v = 0; v < 3; ++v) m *= std::pow(pv.points[i][v], fn.den.basis[k][v]);
+      q += fn.den.coeffs[k] * m;
+    }
+    worst = std::max(worst, std::fabs(p / q - pv.values[i]) / std::max(1.0, std::fabs(pv.values[i])));
+  }
+  CHECK(worst < 1e-8);
+  CHECK(fitted.second.numerical_rank >= 4);
+  // fit_all_metrics over a SampleSet (pipeline.hpp:145-184).
+  data::SampleSet set;
+  set.metric_names = {"comp_insts_per_thread"};
+  for (size_t i = 0; i < pv.points.size(); ++i) {
+    data::Sample smp;
+    smp.data_params = {(long long)pv.points[i][0]};
+    smp.config = perf::LaunchConfig{(long long)pv.points[i][1], (long long)pv.points[i][2], 1};
+    smp.metric_values["comp_insts_per_thread"] = pv.values[i];
+    set.samples.push_back(smp);
+  }
+  auto ms = pipe::fit_all_metrics(set, {{"comp_insts_per_thread", fb}}, {{"regs_per_thread", 20.0}});
+  CHECK(ms.variables == (std::vector<std::string>{"D1", "bx", "by"}));
+  CHECK(ms.models.count("comp_insts_per_thread") == 1 && ms.failures.empty());
+  CHECK(throws_with<pipe::PipelineError>(
+      [&] { pipe::fit_all_metrics(set, {}, {{"comp_insts_per_thread", 1.0}}); }, "both a sample column"));
 }
 
 int main(int argc, char** argv) {
