@@ -433,13 +433,69 @@ def gpu_arm(args):
     return 0
 
 
+def dump_arm(args):
+    """Ec-table dump (BASELINE.md §3 last row): rpg_evaluate_device writes the
+    full per-point table — f64 Ec + u8 case tag + i32 occupancy warps, 13 B per
+    point — for the C2 2DCONV model over 8,192 consecutive N x 7,262 configs
+    (59.5 M points, 773 MB per step).  Reported as HBM GB/s against the
+    measured copy bandwidth; the point model bounds it, not HBM."""
+    import torch
+    from paper_1906_00142_b200 import search as S
+    torch.cuda.set_device(0)
+    wl = Workload("c2")
+    spec = wl.specs["2dconv"]
+    n = 8192
+    data = torch.arange(N0, N0 + n, dtype=torch.int64, device="cuda").reshape(n, 1)
+    pts = n * len(wl.space)
+    ec = torch.empty(pts, dtype=torch.float64, device="cuda")
+    tag = torch.empty(pts, dtype=torch.uint8, device="cuda")
+    wocc = torch.empty(pts, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+    with S.Plan(spec, wl.hw, wl.space, S.SearchOptions(arith=args.arith)) as plan:
+        run = lambda: plan.evaluate_device(data.data_ptr(), n, 1, ec.data_ptr(), tag.data_ptr(),
+                                           wocc.data_ptr(), stream.cuda_stream)
+        for _ in range(max(3, args.warmup)):
+            run()
+        torch.cuda.synchronize()
+        times = []
+        with ClockSampler(0) as clocks:
+            for _ in range(args.steps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                run()
+                e1.record(stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
+    nbytes = pts * 13
+    gbs = nbytes / (ms / 1e3) / 1e9
+    peak = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = json.load(f)["hbm_gbs"]
+    except (OSError, KeyError, ValueError):
+        pass
+    print(json.dumps({
+        "metric": "Ec-table dump bandwidth", "value": gbs, "unit": "GB/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 2DCONV model, N = 64..8255 x 7262 integer (bx,by): Ec f64 + tag u8 + "
+                               "occupancy i32 per point (13 B)", "points": pts, "bytes_per_step": nbytes,
+                   "points_per_s": pts / (ms / 1e3), "arith": args.arith},
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                     "frac": (gbs / peak) if peak else None, "traffic": None,
+                     "note": "store traffic of the evaluate kernel; the FP64 point model, not HBM, bounds it"},
+        "gpu_launches": args.steps, "clocks": clocks.summary()}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c2", "c3", "c5"], default="c2",
+    ap.add_argument("--workload", choices=["c2", "c3", "c5", "dump"], default="c2",
                     help="BASELINE.json config: c2 (default, configs[1]), c3 (full suite), c5 (stress)")
     ap.add_argument("--arith", choices=["exact", "fast"], default="fast")
     ap.add_argument("--kernel", choices=["specialized", "generic"], default="specialized")
@@ -450,7 +506,11 @@ def main():
                     help="test mode: all ranks on cuda:0 (with --dist-backend gloo)")
     args = ap.parse_args()
     if args.impl == "reference":
+        if args.workload == "dump":
+            args.workload = "c2"
         return reference_arm(args)
+    if args.workload == "dump":
+        return dump_arm(args)
     return gpu_arm(args)
 
 
