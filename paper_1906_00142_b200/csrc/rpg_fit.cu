@@ -55,6 +55,7 @@ struct FitParams {
   int64_t m;
   int32_t with_y_col;           // 1: append y as column n (TSQR of [V | y])
   int32_t num_only;             // 1: numerator block only (start-vector LS)
+  const double* Dm;             // optional m x nd raw denominator monomials (den_pass)
 };
 
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
@@ -484,6 +485,18 @@ struct CtlSrc {
   const double* S;
 };
 
+// Raw denominator monomials of every sample (m x nd), computed once per fit
+// and read by every sample pass of the safeguard instead of recomputed.
+__global__ void den_monomials(const FitParams F, double* __restrict__ Dm) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < F.m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double x[RPG_MAX_VARS];
+    for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
+    for (int k = 0; k < F.nd; ++k)
+      Dm[r * F.nd + k] = monomial(x, F.exps + (size_t)(F.nn + k) * F.n_vars, F.n_vars);
+  }
+}
+
 // NDT: compile-time bound on nd (8 = the default (1,1,1) denominator basis)
 // so the per-row monomials and accumulators stay in registers.
 template <int NDT>
@@ -519,11 +532,14 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
     }
   }
   __syncthreads();
-  double qmin[kAlphas], slog[kAlphas];
+  double qmin[kAlphas], slog[kAlphas], prod[kAlphas];
+  int pexp[kAlphas];
 #pragma unroll
   for (int a = 0; a < kAlphas; ++a) {
     qmin[a] = INFINITY;
     slog[a] = 0.0;
+    prod[a] = 1.0;
+    pexp[a] = 0;
   }
   // Gram accumulators: with nd*nd <= blockDim/2 every entry gets `parts`
   // threads (thread = part * nd*nd + entry); else thread t owns entries t,
@@ -541,11 +557,17 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
     const bool valid = threadIdx.x < kPassRows && r < F.m;
     double D[NDT];
     if (valid) {
-      double x[RPG_MAX_VARS];
+      if (F.Dm) {
+        // Denominator monomials precomputed once per fit (m x nd).
 #pragma unroll
-      for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
+        for (int k = 0; k < NDT; ++k) D[k] = k < nd ? F.Dm[r * nd + k] : 0.0;
+      } else {
+        double x[RPG_MAX_VARS];
 #pragma unroll
-      for (int k = 0; k < NDT; ++k) D[k] = k < nd ? monomial(x, sexps + k * F.n_vars, F.n_vars) : 0.0;
+        for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
+#pragma unroll
+        for (int k = 0; k < NDT; ++k) D[k] = k < nd ? monomial(x, sexps + k * F.n_vars, F.n_vars) : 0.0;
+      }
 #pragma unroll
       for (int a = 0; a < kAlphas; ++a) {
         if (a < n_alpha) {
@@ -554,9 +576,21 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
           for (int k = 0; k < NDT; ++k)
             if (k < nd) q = fma(D[k], cands[a * nd + k], q);
           qmin[a] = fmin(qmin[a], q);
-          slog[a] += log(q);
+          // sum log q as log(prod of mantissas) + (sum of exponents) ln 2:
+          // one multiply per row instead of a log (q <= 0 makes it NaN, as
+          // the log would; such candidates fail the q > 0 test anyway).
+          int e;
+          const double mq = frexp(q, &e);
+          prod[a] *= mq;
+          pexp[a] += e;
         }
       }
+    }
+#pragma unroll
+    for (int a = 0; a < kAlphas; ++a) {  // keep the running products in range
+      int e;
+      prod[a] = frexp(prod[a], &e);
+      pexp[a] += e;
     }
     if (newton) {
       __syncthreads();
@@ -613,6 +647,8 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
       gacc[0] = t;
     }
   }
+#pragma unroll
+  for (int a = 0; a < kAlphas; ++a) slog[a] = fma((double)pexp[a], 0.69314718055994530942, log(prod[a]));
   double* out = partial + (size_t)blockIdx.x * (2 * kAlphas + nd + nd * nd);
 #pragma unroll
   for (int a = 0; a < kAlphas; ++a) {
@@ -868,7 +904,7 @@ __device__ __forceinline__ void ctl_end_inner(MinCtl* ctl) {
 //           accept the first (in halving order) with q > 0 and Armijo
 //           decrease, else continue halving (the inner loop ends when alpha
 //           drops to 1e-18) — polyfit.hpp:279-306.
-__device__ __forceinline__ void ctl_step_body(const double* __restrict__ R, const double* __restrict__ S,
+__device__ __forceinline__ void ctl_step_body(const double* R, const double* __restrict__ S,
                                               const double* __restrict__ gsum,
                                               const double* __restrict__ pass_out,
                                               double* __restrict__ c, int nn, int nd,
@@ -877,6 +913,16 @@ __device__ __forceinline__ void ctl_step_body(const double* __restrict__ R, cons
   const int ph = ctl->phase;
   if (ph >= kMinDone) return;
   const int n = nn + nd;
+  // Stage R (n x n) in SMEM behind newton_body's KKT workspace: every dot
+  // product below reads it many times.
+  {
+    extern __shared__ __align__(16) double fsm[];
+    double* Rs = fsm + (n + 1) * (n + 2) + 3 * n;
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) Rs[e] = R[e];
+    __syncthreads();
+    R = Rs;
+  }
   if (ph == kMinNewton) {
     newton_body(R, S, gsum, pass_out, c, nn, nd, dc, ctl->mu, scratch);
     __syncthreads();
@@ -953,28 +999,49 @@ __device__ __forceinline__ void ctl_step_body(const double* __restrict__ R, cons
 }
 
 // One whole minimizer step in one launch: every CTA runs its share of the
-// controlled sample pass; the last CTA to finish (threadfence + counter)
-// reduces the partials and applies the Newton / line-search update, then
-// re-arms the counter.  No-op for every CTA once the loop is done.
+// controlled sample pass and writes its partial sums; the partials are
+// folded in two deterministic levels — the last CTA of each group of
+// kStepGroup CTAs (threadfence + per-group counter) reduces its group, the
+// last group reducer reduces the group sums — and that CTA applies the
+// Newton / line-search update and re-arms the counters.  Every reduction
+// follows lane / shuffle order, so the result does not depend on which CTA
+// arrives last.  No-op for every CTA once the loop is done.
+constexpr int kStepGroup = 32;
+
 template <int NDT>
 __global__ void __launch_bounds__(kFitThreads)
 min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __restrict__ pass_out,
-         unsigned* __restrict__ counter, const double* __restrict__ R, const double* __restrict__ S,
+         unsigned* __restrict__ counter /* n_groups + 1 */, double* __restrict__ gpart,
+         const double* __restrict__ R, const double* __restrict__ S,
          const double* __restrict__ gsum, double* __restrict__ c, double* __restrict__ dc,
          MinCtl* __restrict__ ctl, MinState* __restrict__ scratch) {
   if (src.ctl->phase >= kMinDone) return;
   den_pass_body<NDT>(F, nullptr, nullptr, nullptr, 1, 1, partial, src);
+  const int W = 2 * kAlphas + F.nd + F.nd * F.nd;
+  const int G = gridDim.x, n_groups = (G + kStepGroup - 1) / kStepGroup;
+  const int group = blockIdx.x / kStepGroup;
+  const int gsize = min(kStepGroup, G - group * kStepGroup);
   __shared__ int last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(counter + group, 1u) == (unsigned)gsize - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  den_pass_reduce(partial, gridDim.x, F.nd, pass_out);
+  den_pass_reduce(partial + (size_t)group * kStepGroup * W, gsize, F.nd, gpart + (size_t)group * W);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    counter[group] = 0u;
+    last = atomicAdd(counter + n_groups, 1u) == (unsigned)n_groups - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  den_pass_reduce(gpart, n_groups, F.nd, pass_out);
   __syncthreads();
   ctl_step_body(R, S, gsum, pass_out, c, F.nn, F.nd, dc, ctl, scratch);
-  if (threadIdx.x == 0) *counter = 0u;
+  if (threadIdx.x == 0) counter[n_groups] = 0u;
 }
 
 __global__ void to_raw(const double* __restrict__ c, const double* __restrict__ S, int n,
@@ -1215,7 +1282,8 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   FCUDA(cudaMemcpyAsync(&hs, st.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
   FCUDA(cudaStreamSynchronize(s));
   if (!hs.ok) return RPG_OK;
-  const size_t smk = sizeof(double) * ((size_t)(kMaxCols + 1) * (kMaxCols + 2) + 3 * kMaxCols);
+  // newton_body's KKT workspace + the staged R (ctl_step_body)
+  const size_t smk = sizeof(double) * ((size_t)(n + 1) * (n + 2) + 3 * (size_t)n + (size_t)n * n);
   DevBuf ctlb;
   FCUDA(cudaMalloc(&ctlb.p, sizeof(MinCtl)));
   MinCtl hc{};
@@ -1224,9 +1292,12 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   hc.n_alpha = 1;
   FCUDA(cudaMemcpyAsync(ctlb.p, &hc, sizeof(hc), cudaMemcpyHostToDevice, s));
   MinCtl* dctl = ctlb.as<MinCtl>();
-  DevBuf counter;
-  FCUDA(cudaMalloc(&counter.p, sizeof(unsigned)));
-  FCUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), s));
+  const int n_groups = (P.G + kStepGroup - 1) / kStepGroup;
+  const int Wp = 2 * kAlphas + nd + nd * nd;
+  DevBuf counter, gpart;
+  FCUDA(cudaMalloc(&counter.p, sizeof(unsigned) * (n_groups + 1)));
+  FCUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned) * (n_groups + 1), s));
+  FCUDA(cudaMalloc(&gpart.p, sizeof(double) * (size_t)n_groups * Wp));
   const size_t smstep = std::max(smk, den_pass_smem(F));
   FCUDA(cudaFuncSetAttribute(min_step<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smstep));
   FCUDA(cudaFuncSetAttribute(min_step<kMaxCols>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1240,12 +1311,13 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
     for (int i = 0; i < kChunk; ++i) {
       if (F.nd <= 8)
         min_step<8><<<P.G, kFitThreads, smstep, s>>>(F, src, P.part.as<double>(), P.out.as<double>(),
-                                                     counter.as<unsigned>(), R, S, gsum, c.as<double>(),
-                                                     dc.as<double>(), dctl, st.as<MinState>());
+                                                     counter.as<unsigned>(), gpart.as<double>(), R, S,
+                                                     gsum, c.as<double>(), dc.as<double>(), dctl,
+                                                     st.as<MinState>());
       else
         min_step<kMaxCols><<<P.G, kFitThreads, smstep, s>>>(
-            F, src, P.part.as<double>(), P.out.as<double>(), counter.as<unsigned>(), R, S, gsum,
-            c.as<double>(), dc.as<double>(), dctl, st.as<MinState>());
+            F, src, P.part.as<double>(), P.out.as<double>(), counter.as<unsigned>(), gpart.as<double>(),
+            R, S, gsum, c.as<double>(), dc.as<double>(), dctl, st.as<MinState>());
     }
     FCUDA(cudaGetLastError());
     FCUDA(cudaMemcpyAsync(&hc, ctlb.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
@@ -1266,9 +1338,20 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
 
 // The positivity safeguard (polyfit.hpp:369-414).  c: in = the unconstrained
 // candidate (raw coordinates), out = the refined vector when one is found.
-int rpg_fit_safeguard(const FitParams& F, const double* R, const double* S, double* c,
+int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, double* c,
                       double rank_tol, int sms, cudaStream_t s, char* err, size_t errlen) {
-  const int nn = F.nn, nd = F.nd, n = F.n;
+  const int nn = F0.nn, nd = F0.nd, n = F0.n;
+  // The sample passes read precomputed denominator monomials.
+  DevBuf dm;
+  FitParams F = F0;
+  if (cudaMalloc(&dm.p, sizeof(double) * (size_t)F0.m * nd) == cudaSuccess) {
+    den_monomials<<<(int)std::min<int64_t>((F0.m + 255) / 256, 8LL * sms), 256, 0, s>>>(
+        F0, dm.as<double>());
+    FCUDA(cudaGetLastError());
+    F.Dm = dm.as<double>();
+  } else {
+    cudaGetLastError();  // out of memory: recompute the monomials per pass
+  }
   DevBuf gpart, gsum, Rvy, Rv, z, sv, Wv, Uv, dummy, start, refined, next, w, Rw, Sw;
   // column sums of the raw denominator monomials
   const int G = std::max(1, std::min<int>((int)((F.m + 255) / 256), 2 * sms));
