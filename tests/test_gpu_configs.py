@@ -113,3 +113,30 @@ def test_c5_stress_sampled(arith):
     grid = np.stack([nn.ravel(), mm.ravel()], axis=1)
     data = np.ascontiguousarray(grid[:: 33124 // 24][:24])
     _check(_models("stencil3d_nm", "stress"), _b200(), F.integer_configs(1024, dims=3), data, arith)
+
+
+@pytest.mark.parametrize("kernel", ["2dconv", "gemm", "atax1"])
+def test_c2_fast_agrees_with_reference_order(kernel):
+    """The benchmark's FAST arithmetic against the reference's operation
+    order (O1 EXACT) at the north star's tolerance: the FAST winner equals
+    the EXACT winner, or its EXACT cycle estimate is within 1e-9 (relative)
+    of the EXACT minimum (ties within the tolerance count as agreement)."""
+    spec, hw = _models(kernel), _b200()
+    space = F.integer_configs(1024, dims=2)
+    data = np.arange(64, 65537, 7, dtype=np.int64).reshape(-1, 1)
+    pk = A.PackedModel(spec, drop_zero_terms=False)
+    sp = A.config_array(space)
+    exact = o1.search_batch(pk, A.profile_struct(hw), A.options_struct(arith=A.RPG_ARITH_EXACT), sp, data,
+                            _threads())
+    with S.Plan(spec, hw, space, S.SearchOptions(arith="fast")) as plan:
+        fast = plan.search_batch(data)
+    diff = np.nonzero(fast["cfg_idx"] != exact["cfg_idx"])[0]
+    if len(diff):
+        ec, _, _ = o1.evaluate_batch(pk, A.profile_struct(hw), A.options_struct(arith=A.RPG_ARITH_EXACT), sp,
+                                     np.ascontiguousarray(data[diff]), _threads())
+        for j, t in enumerate(diff):
+            row = ec[j]
+            best = row[row >= 0].min()
+            assert row[fast["cfg_idx"][t]] <= best * (1 + 1e-9), (int(data[t, 0]), best)
+    rel = np.abs(fast["best_ec"] - exact["best_ec"]) / np.maximum(1.0, np.abs(exact["best_ec"]))
+    assert rel.max() <= 1e-9
