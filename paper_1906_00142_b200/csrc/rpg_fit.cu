@@ -475,6 +475,8 @@ struct MinCtl {
   int phase, outer, inner, n_alpha;
   double mu, phi0, decrement, alpha;  // alpha: first candidate of the next line pass
   double al[kAlphas];
+  long long tail_cycles[2];           // RPG_FIT_TRACE: serial tail time (Newton, line)
+  int n_steps[2];
 };
 // Candidate source of a controlled den_pass: c, dc in equilibrated
 // coordinates, S the column scale.
@@ -485,6 +487,21 @@ struct CtlSrc {
   const double* S;
 };
 
+// frexp for the running log-sum products: integer exponent split on the
+// high word for normal numbers, frexp otherwise (zero, subnormal, inf, NaN).
+__device__ __forceinline__ double split_mant(double q, int& e) {
+  const int hi = __double2hiint(q);
+  const int ex = (hi >> 20) & 0x7ff;
+  if (ex > 0 && ex < 0x7ff) {
+    e += ex - 1022;
+    return __hiloint2double((hi & 0x800fffff) | (1022 << 20), __double2loint(q));
+  }
+  int e2;
+  const double m = frexp(q, &e2);
+  e += e2;
+  return m;
+}
+
 // Raw denominator monomials of every sample (m x nd), computed once per fit
 // and read by every sample pass of the safeguard instead of recomputed.
 __global__ void den_monomials(const FitParams F, double* __restrict__ Dm) {
@@ -492,8 +509,9 @@ __global__ void den_monomials(const FitParams F, double* __restrict__ Dm) {
        r += (int64_t)gridDim.x * blockDim.x) {
     double x[RPG_MAX_VARS];
     for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
-    for (int k = 0; k < F.nd; ++k)
-      Dm[r * F.nd + k] = monomial(x, F.exps + (size_t)(F.nn + k) * F.n_vars, F.n_vars);
+    const int st = F.nd <= 8 ? 8 : F.nd;  // stride 8 (zero-padded) for den_pass<8>
+    for (int k = 0; k < st; ++k)
+      Dm[r * st + k] = k < F.nd ? monomial(x, F.exps + (size_t)(F.nn + k) * F.n_vars, F.n_vars) : 0.0;
   }
 }
 
@@ -515,13 +533,33 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
     newton = ph == kMinNewton;
     n_alpha = newton ? 1 : src.ctl->n_alpha;
   }
-  double* U = fsm;                                  // kPassRows x nd (row-major)
-  double* red = U + kPassRows * nd;                 // 32
-  double* cands = red + 32;                         // kAlphas x nd
-  uint8_t* sexps = reinterpret_cast<uint8_t*>(cands + kAlphas * nd);
+  double* U = fsm;                                  // kPassRows x ust (row-major)
+  const int ust = NDT == 8 ? 8 : nd;                // row stride (8: padded for the DMMA Gram)
+  double* red = U + kPassRows * ust;                // 32
+  double* cands = red + 32;                         // kAlphas x nd (NDT == 8: cd[8], dd[8])
+  uint8_t* sexps = reinterpret_cast<uint8_t*>(cands + kAlphas * (nd > 4 ? nd : 4));
   for (int e = threadIdx.x; e < nd * F.n_vars; e += blockDim.x)
     sexps[e] = F.exps[F.nn * F.n_vars + e];
-  for (int e = threadIdx.x; e < n_alpha * nd; e += blockDim.x) {
+  double al[kAlphas] = {0.0, 0.0, 0.0, 0.0};
+  bool has_dir = false;
+  if constexpr (NDT == 8) {
+    // q_a = D.(cd + al_a dd) evaluated as D.cd + al_a (D.dd): two dot products
+    // per row for all candidates.
+    has_dir = src.ctl ? !newton : dd != nullptr;
+#pragma unroll
+    for (int a = 0; a < kAlphas; ++a)
+      al[a] = a < n_alpha ? (src.ctl ? src.ctl->al[a] : (alphas ? alphas[a] : 0.0)) : 0.0;
+    if (threadIdx.x < 16) {
+      const int k = threadIdx.x & 7;
+      double v = 0.0;
+      if (k < nd) {
+        if (threadIdx.x < 8) v = src.ctl ? src.S[F.nn + k] * src.c[F.nn + k] : cd[k];
+        else if (has_dir) v = src.ctl ? src.S[F.nn + k] * src.dc[F.nn + k] : dd[k];
+      }
+      cands[threadIdx.x] = v;
+    }
+  }
+  for (int e = threadIdx.x; NDT != 8 && e < n_alpha * nd; e += blockDim.x) {
     const int a = e / nd, k = e % nd;
     if (src.ctl) {
       const int j = F.nn + k;
@@ -551,12 +589,44 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
 #pragma unroll
   for (int i = 0; i < (NDT <= 8 ? 1 : 16); ++i) gacc[i] = 0.0;
   double gq = 0.0;  // thread t < nd owns sum (1/q) D[t]
+  double gmma0 = 0.0, gmma1 = 0.0, gqv = 0.0;  // NDT == 8: DMMA accumulator fragment, column sums
   const int64_t nrow_tiles = (F.m + kPassRows - 1) / kPassRows;
   for (int64_t tile = blockIdx.x; tile < nrow_tiles; tile += gridDim.x) {
     const int64_t r = tile * kPassRows + threadIdx.x;
     const bool valid = threadIdx.x < kPassRows && r < F.m;
     double D[NDT];
-    if (valid) {
+    if (NDT == 8 && valid) {
+      if (F.Dm) {
+        const double2* row = reinterpret_cast<const double2*>(F.Dm + r * 8);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 v = row[k];
+          D[2 * k] = v.x;
+          D[2 * k + 1] = v.y;
+        }
+      } else {
+        double x[RPG_MAX_VARS];
+#pragma unroll
+        for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
+#pragma unroll
+        for (int k = 0; k < NDT; ++k) D[k] = k < nd ? monomial(x, sexps + k * F.n_vars, F.n_vars) : 0.0;
+      }
+      double q0 = 0.0, qd = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) q0 = fma(D[k], cands[k], q0);
+      if (has_dir) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) qd = fma(D[k], cands[8 + k], qd);
+      }
+#pragma unroll
+      for (int a = 0; a < kAlphas; ++a) {
+        if (a < n_alpha) {
+          const double q = has_dir ? fma(al[a], qd, q0) : q0;
+          qmin[a] = fmin(qmin[a], q);
+          prod[a] *= split_mant(q, pexp[a]);
+        }
+      }
+    } else if (valid) {
       if (F.Dm) {
         // Denominator monomials precomputed once per fit (m x nd).
 #pragma unroll
@@ -587,11 +657,7 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
       }
     }
 #pragma unroll
-    for (int a = 0; a < kAlphas; ++a) {  // keep the running products in range
-      int e;
-      prod[a] = frexp(prod[a], &e);
-      pexp[a] += e;
-    }
+    for (int a = 0; a < kAlphas; ++a) prod[a] = split_mant(prod[a], pexp[a]);  // keep products in range
     if (newton) {
       __syncthreads();
       if (threadIdx.x < kPassRows) {
@@ -599,14 +665,34 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
         if (valid) {
 #pragma unroll
           for (int k = 0; k < NDT; ++k)
-            if (k < nd) q = fma(D[k], cands[k], q);
+            if (NDT == 8 || k < nd) q = fma(D[k], cands[k], q);
           qi = 1.0 / q;
         }
+        if constexpr (NDT == 8) {
+          // stride 8, zero-padded past nd (the DMMA Gram below)
 #pragma unroll
-        for (int k = 0; k < NDT; ++k)
-          if (k < nd) U[threadIdx.x * nd + k] = valid ? D[k] * qi : 0.0;
+          for (int k = 0; k < 8; ++k) U[threadIdx.x * 8 + k] = (valid && k < nd) ? D[k] * qi : 0.0;
+        } else {
+#pragma unroll
+          for (int k = 0; k < NDT; ++k)
+            if (k < nd) U[threadIdx.x * nd + k] = valid ? D[k] * qi : 0.0;
+        }
       }
       __syncthreads();
+      if constexpr (NDT == 8) {
+        // Gram U^T U and column sums on the FP64 tensor cores: warp w folds
+        // rows [32w, 32w + 32) in 4-row chunks with mma.m8n8k4 (A = U^T
+        // chunk, B = U chunk: lane l supplies U[r0 + l%4][l/4] to both).
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+        for (int cidx = 0; cidx < 8; ++cidx) {
+          const double v = U[(warp * 32 + cidx * 4 + (lane & 3)) * 8 + (lane >> 2)];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(gmma0), "+d"(gmma1) : "d"(v), "d"(v));
+          gqv += v;
+        }
+        continue;
+      }
       // Gram of the tile's U rows: `parts` threads per entry, each over a
       // contiguous row range with four independent accumulators.
       for (int e = threadIdx.x % ne_stride, i = 0; part < parts && e < nd * nd; e += ne_stride, ++i) {
@@ -635,7 +721,28 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
       }
     }
   }
-  if (newton && parts > 1) {
+  if constexpr (NDT == 8) {
+    if (newton) {
+      // Fold the 8 warps' fragments (fixed order): thread t holds
+      // G[t/4][2(t%4) + {0,1}] of its warp; column sums by column t/4.
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      gqv += __shfl_xor_sync(0xffffffffu, gqv, 1);
+      gqv += __shfl_xor_sync(0xffffffffu, gqv, 2);
+      __syncthreads();
+      double* Pm = U;  // reuse: 8 warps x (64 Gram + 8 column sums)
+      Pm[warp * 72 + (lane >> 2) * 8 + 2 * (lane & 3)] = gmma0;
+      Pm[warp * 72 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = gmma1;
+      if ((lane & 3) == 0) Pm[warp * 72 + 64 + (lane >> 2)] = gqv;
+      __syncthreads();
+      if (threadIdx.x < 72) {
+        double t = 0.0;
+        for (int w = 0; w < kFitWarps; ++w) t += Pm[w * 72 + threadIdx.x];
+        if (threadIdx.x < 64) gacc[0] = t;
+        else gq = t;
+      }
+    }
+  }
+  if (newton && parts > 1 && NDT != 8) {
     // Fold the per-part partial Gram entries (thread = part * ne + entry).
     __syncthreads();
     double* P = U;  // reuse: parts x nd*nd
@@ -673,7 +780,11 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
       out[2 * a + 1] = sm;
     }
   }
-  if (newton) {
+  if (newton && NDT == 8) {
+    const int t = threadIdx.x;
+    if (t < 64 && (t >> 3) < nd && (t & 7) < nd) out[2 * kAlphas + nd + (t >> 3) * nd + (t & 7)] = gacc[0];
+    if (t >= 64 && t < 64 + nd) out[2 * kAlphas + (t - 64)] = gq;
+  } else if (newton) {
     if ((int)threadIdx.x < nd) out[2 * kAlphas + threadIdx.x] = gq;
     if (parts > 1) {
       if ((int)threadIdx.x < nd * nd) out[2 * kAlphas + nd + threadIdx.x] = gacc[0];
@@ -809,13 +920,15 @@ __device__ void newton_body(const double* __restrict__ R, const double* __restri
     K[n * (N + 1) + N] = 0.0;
   }
   __syncthreads();
+  __shared__ int singular;
+  __shared__ double xs[kMaxCols + 1];
+  if (threadIdx.x == 0) singular = 0;
+  {
   // Gaussian elimination with partial pivoting: warp 0 picks the pivot (the
   // first row holding the largest |entry|, as a sequential scan would), the
   // multipliers are formed once per row, all threads eliminate.
   __shared__ int piv;
-  __shared__ int singular;
   __shared__ double mult[kMaxCols + 1];
-  __shared__ double xs[kMaxCols + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) singular = 0;
   for (int col = 0; col < N; ++col) {
@@ -870,6 +983,7 @@ __device__ void newton_body(const double* __restrict__ R, const double* __restri
     }
   }
   __syncthreads();
+  }
   if (threadIdx.x == 0) {
     const double* x = xs;
     bool finite = !singular;
@@ -917,7 +1031,7 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
   // product below reads it many times.
   {
     extern __shared__ __align__(16) double fsm[];
-    double* Rs = fsm + (n + 1) * (n + 2) + 3 * n;
+    double* Rs = fsm + (n + 1) * (n + 2) + 3 * n;  // behind newton_body's workspace
     __syncthreads();
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) Rs[e] = R[e];
     __syncthreads();
@@ -1038,10 +1152,17 @@ min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __
   __syncthreads();
   if (!last) return;
   __threadfence();
+  const long long t0 = clock64();
+  const int ph = ctl->phase;
   den_pass_reduce(gpart, n_groups, F.nd, pass_out);
   __syncthreads();
   ctl_step_body(R, S, gsum, pass_out, c, F.nn, F.nd, dc, ctl, scratch);
-  if (threadIdx.x == 0) counter[n_groups] = 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    counter[n_groups] = 0u;
+    ctl->tail_cycles[ph == kMinNewton ? 0 : 1] += clock64() - t0;
+    ctl->n_steps[ph == kMinNewton ? 0 : 1] += 1;
+  }
 }
 
 __global__ void to_raw(const double* __restrict__ c, const double* __restrict__ S, int n,
@@ -1215,7 +1336,8 @@ int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, c
 }  // namespace
 
 size_t den_pass_smem(const FitParams& F) {
-  return sizeof(double) * ((size_t)kPassRows * F.nd + 32 + kAlphas * F.nd) +
+  const size_t ust = F.nd <= 8 ? 8 : (size_t)F.nd;
+  return sizeof(double) * ((size_t)kPassRows * ust + 32 + kAlphas * (size_t)std::max(F.nd, 4)) +
          (size_t)F.nd * RPG_MAX_VARS + 16;
 }
 
@@ -1324,8 +1446,12 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
     FCUDA(cudaStreamSynchronize(s));
     done = hc.phase >= kMinDone;
     if (done && getenv("RPG_FIT_TRACE"))
-      fprintf(stderr, "[rpg_fit] minimizer: <= %d steps, phase %d, outer %d, inner %d\n",
-              steps + kChunk, hc.phase, hc.outer, hc.inner);
+      fprintf(stderr,
+              "[rpg_fit] minimizer: %d Newton + %d line steps, phase %d, outer %d; serial tail "
+              "%.1f / %.1f us per Newton / line step\n",
+              hc.n_steps[0], hc.n_steps[1], hc.phase, hc.outer,
+              hc.n_steps[0] ? hc.tail_cycles[0] / 1965.0 / hc.n_steps[0] : 0.0,
+              hc.n_steps[1] ? hc.tail_cycles[1] / 1965.0 / hc.n_steps[1] : 0.0);
   }
   if (hc.phase == kMinFail) return RPG_OK;
   to_raw<<<1, 32, 0, s>>>(c.as<double>(), S, n, out_raw, fin.as<int>());
@@ -1344,7 +1470,8 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
   // The sample passes read precomputed denominator monomials.
   DevBuf dm;
   FitParams F = F0;
-  if (cudaMalloc(&dm.p, sizeof(double) * (size_t)F0.m * nd) == cudaSuccess) {
+  static const bool use_dm = getenv("RPG_FIT_NO_DM") == nullptr;
+  if (use_dm && cudaMalloc(&dm.p, sizeof(double) * (size_t)F0.m * (nd <= 8 ? 8 : nd)) == cudaSuccess) {
     den_monomials<<<(int)std::min<int64_t>((F0.m + 255) / 256, 8LL * sms), 256, 0, s>>>(
         F0, dm.as<double>());
     FCUDA(cudaGetLastError());

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--noise", type=float, default=0.0)
     ap.add_argument("--cpu", action="store_true", help="also time oracle O3 (slow)")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--no-warmup", action="store_true", help="skip the small warm-up fit (profiling)")
     args = ap.parse_args()
     from paper_1906_00142_b200 import fit as G
     from paper_1906_00142_b200 import formats as F
@@ -45,10 +46,11 @@ def main():
         ys[name] = np.ascontiguousarray(y)
     nb, db = [2, 2, 2], [1, 1, 1]
     # warm-up (context, module load)
-    try:
-        G.fit_rational(X[:4096], ys[F.METRIC_COMP][:4096], spec.variables, nb, db)
-    except (G.DegenerateFit, G.SvdFailure):
-        pass
+    if not args.no_warmup:
+        try:
+            G.fit_rational(X[:4096], ys[F.METRIC_COMP][:4096], spec.variables, nb, db)
+        except (G.DegenerateFit, G.SvdFailure):
+            pass
     times, safeguards = [], {}
     for _ in range(args.reps):
         t0 = time.perf_counter()
