@@ -21,24 +21,24 @@ struct Module {
 // default for tuning sweeps) and the resident CTAs per SM their register
 // budget targets (RPG_JIT_MIN_BLOCKS overrides).
 constexpr int kDefaultThreads = 32;
-int jit_threads();
-int default_min_blocks();
+int jit_threads(bool exact = false);
+int default_min_blocks(int threads);
 
 // CUDA source of the specialized kernels for a plan's model.
 std::string generate_source(const rpg::Params& P, const std::vector<double>& coef,
                             const std::vector<uint64_t>& exps, bool fast, bool two_point = false);
 
 // NVRTC -> sm_100a cubin.
-int compile(const std::string& source, int min_blocks, std::vector<char>* cubin,
+int compile(const std::string& source, int min_blocks, int threads, std::vector<char>* cubin,
             std::string* log);
 
 // Generates, compiles (cached per process by source) and loads.
 int get_module(const rpg::Params& P, const std::vector<double>& coef,
                const std::vector<uint64_t>& exps, bool fast, int device, int min_blocks,
-               Module* out, std::string* err);
+               int threads, Module* out, std::string* err);
 
 // Same, for an already generated source.
-int get_module_src(const std::string& src, int device, int min_blocks, Module* out,
+int get_module_src(const std::string& src, int device, int min_blocks, int threads, Module* out,
                    std::string* err);
 
 // Specialized kernels for a bare rational program (rpg_program.cu).

@@ -458,9 +458,10 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     std::string jerr;
     // Resident CTAs per SM the specialized kernels are register-budgeted for
     // (launch bounds); RPG_JIT_MIN_BLOCKS overrides it for tuning sweeps.
-    if (jit(rpg_jit::default_min_blocks(), &plan->jit, &jerr) != 0)
+    const int threads = rpg_jit::jit_threads(!is_program && P.arith == RPG_ARITH_EXACT);
+    if (jit(rpg_jit::default_min_blocks(threads), threads, &plan->jit, &jerr) != 0)
       return fail(set_err(err, errlen, RPG_E_CUDA, "%s", jerr.c_str()));
-    plan->threads = rpg_jit::jit_threads();
+    plan->threads = threads;
   }
   auto setup = [&](const void* fn, int* grid) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -625,9 +626,9 @@ int rpg_plan_create(const rpg_model* model, const rpg_profile* hw, const rpg_con
   const bool fast = P.arith == RPG_ARITH_FAST;
   return build_plan(P, tab, space, n_space, device, fast,
                     opts->kernel == RPG_KERNEL_SPECIALIZED, false,
-                    [&](int min_blocks, rpg_jit::Module* m, std::string* jerr) {
+                    [&](int min_blocks, int threads, rpg_jit::Module* m, std::string* jerr) {
                       return rpg_jit::get_module(P, tab.coef, tab.exps, fast, device,
-                                                 min_blocks, m, jerr);
+                                                 min_blocks, threads, m, jerr);
                     },
                     out, err, errlen);
 }
@@ -645,10 +646,10 @@ int rpg_program_plan_create(const rpg_program* prog, const rpg_profile* hw,
   if ((rc = prepare_program(prog, hw, opts, P, tab, err, errlen))) return rc;
   const rpg_program prog_copy = *prog;
   rc = build_plan(P, tab, space, n_space, device, false, true, true,
-                  [&](int min_blocks, rpg_jit::Module* m, std::string* jerr) {
+                  [&](int min_blocks, int threads, rpg_jit::Module* m, std::string* jerr) {
                     return rpg_jit::get_module_src(
                         rpg_jit::generate_program_source(prog_copy, P), device, min_blocks,
-                        m, jerr);
+                        threads, m, jerr);
                   },
                   out, err, errlen);
   if (rc == RPG_OK) (*out)->step_limit = prog->step_limit;
@@ -894,7 +895,8 @@ extern "C" int64_t rpg_emit_cuda_source(const rpg_model* model, const rpg_profil
   if (compile) {
     std::vector<char> cubin;
     std::string log;
-    if (rpg_jit::compile(src, rpg_jit::default_min_blocks(), &cubin, &log) != 0)
+    const int threads = rpg_jit::jit_threads(opts->arith == RPG_ARITH_EXACT);
+    if (rpg_jit::compile(src, rpg_jit::default_min_blocks(threads), threads, &cubin, &log) != 0)
       return set_err(err, errlen, RPG_E_CUDA, "NVRTC: %s", log.substr(0, 1500).c_str());
     if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
   }
@@ -920,7 +922,8 @@ extern "C" int64_t rpg_emit_program_cuda_source(const rpg_program* prog, const r
   if (compile) {
     std::vector<char> cubin;
     std::string log;
-    if (rpg_jit::compile(src, rpg_jit::default_min_blocks(), &cubin, &log) != 0)
+    const int threads = rpg_jit::jit_threads(false);
+    if (rpg_jit::compile(src, rpg_jit::default_min_blocks(threads), threads, &cubin, &log) != 0)
       return set_err(err, errlen, RPG_E_CUDA, "NVRTC: %s", log.substr(0, 1500).c_str());
     if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
   }
