@@ -151,6 +151,8 @@ struct rpg_plan {
   // host-API staging
   std::mutex mu;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host-API D2H of finished chunks
+  std::vector<cudaEvent_t> chunk_done;
   int64_t* d_data = nullptr;
   size_t d_data_cap = 0;
   void* d_out = nullptr;
@@ -397,6 +399,7 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
   } while (0)
   PLAN_CUDA(cudaSetDevice(device));
   PLAN_CUDA(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+  PLAN_CUDA(cudaStreamCreateWithFlags(&plan->copy_stream, cudaStreamNonBlocking));
   PLAN_CUDA(cudaDeviceGetAttribute(&plan->sm_count, cudaDevAttrMultiProcessorCount, device));
   const size_t nt = std::max<size_t>(coef.size(), 1);
   PLAN_CUDA(cudaMalloc(&plan->d_coef, sizeof(double) * nt));
@@ -607,6 +610,8 @@ int rpg_plan_destroy(rpg_plan* plan) {
   cudaFree(plan->d_data);
   cudaFree(plan->d_out);
   if (plan->stream) cudaStreamDestroy(plan->stream);
+  if (plan->copy_stream) cudaStreamDestroy(plan->copy_stream);
+  for (cudaEvent_t e : plan->chunk_done) cudaEventDestroy(e);
   delete plan;  // specialized modules stay cached for the process
   return RPG_OK;
 }
@@ -734,12 +739,53 @@ int rpg_search_batch(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int3
                              cudaMemcpyHostToDevice, plan->stream));
   if (plan->is_program)
     CUDA_TRY(cudaMemsetAsync(plan->d_err, 0xff, sizeof(unsigned long long), plan->stream));
-  rc = launch_search(plan, plan->d_data, n_tuples, d, (rpg_winner*)plan->d_out, plan->stream,
-                     err, errlen);
-  if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(out, plan->d_out, out_bytes, cudaMemcpyDeviceToHost, plan->stream));
+  // Large batches run as chunks of whole persistent-grid waves so the D2H of
+  // a finished chunk overlaps the kernels of the next ones (no extra tail:
+  // every chunk but the last is an exact multiple of the resident grid).
+  const int64_t chunk = 4LL * std::max(1, plan->grid_search);
+  const int64_t n_chunks = plan->is_program ? 1 : std::max<int64_t>(1, std::min<int64_t>(8, n_tuples / chunk));
+  if (n_chunks <= 1) {
+    rc = launch_search(plan, plan->d_data, n_tuples, d, (rpg_winner*)plan->d_out, plan->stream,
+                       err, errlen);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(out, plan->d_out, out_bytes, cudaMemcpyDeviceToHost, plan->stream));
+    CUDA_TRY(cudaStreamSynchronize(plan->stream));
+    return plan->is_program ? take_program_error(plan, err, errlen) : RPG_OK;
+  }
+  // Chunks of `chunk` tuples, the remainder folded into the second-to-last
+  // chunk, and a last chunk of one wave so the only exposed copy is small.
+  const int64_t wave = std::max(1, plan->grid_search);
+  int64_t lo[10], cnt[10];
+  int64_t nc = 0;
+  for (int64_t at = 0; at < n_tuples;) {
+    const int64_t left = n_tuples - at;
+    int64_t take = left <= wave ? left : (left < chunk + 2 * wave ? left - wave : chunk);
+    if (nc == 8) take = left;
+    lo[nc] = at;
+    cnt[nc] = take;
+    ++nc;
+    at += take;
+  }
+  while ((int64_t)plan->chunk_done.size() < nc) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    plan->chunk_done.push_back(e);
+  }
+  rpg_winner* d_out = (rpg_winner*)plan->d_out;
+  for (int64_t i = 0; i < nc; ++i) {
+    rc = launch_search(plan, plan->d_data + lo[i] * d, cnt[i], d, d_out + lo[i], plan->stream, err,
+                       errlen);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(plan->chunk_done[i], plan->stream));
+  }
+  for (int64_t i = 0; i < nc; ++i) {
+    CUDA_TRY(cudaStreamWaitEvent(plan->copy_stream, plan->chunk_done[i], 0));
+    CUDA_TRY(cudaMemcpyAsync(out + lo[i], d_out + lo[i], sizeof(rpg_winner) * (size_t)cnt[i],
+                             cudaMemcpyDeviceToHost, plan->copy_stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(plan->copy_stream));
   CUDA_TRY(cudaStreamSynchronize(plan->stream));
-  return plan->is_program ? take_program_error(plan, err, errlen) : RPG_OK;
+  return RPG_OK;
 }
 
 int rpg_evaluate_device(rpg_plan* plan, const int64_t* d_data, int64_t n_tuples, int32_t d,
