@@ -865,6 +865,90 @@ __global__ void min_setup(const double* __restrict__ R, const double* __restrict
   st->ok = 1;
 }
 
+// Per-minimizer-call factorization of the Newton matrix's constant part.
+// H = 2 H0 + mu M with H0 = S R^T R S fixed for the call and M nonzero only
+// on the denominator block, so with u = numerator, v = denominator block:
+//   A = 2 H0_uu (Cholesky, explicit inverse), B = 2 H0_uv, F = A^-1 B,
+//   Sv0 = 2 H0_vv - B^T F.
+// A Newton step then only solves the (nd+1) x (nd+1) Schur system
+// [Sv0 + mu M_vv, g_v; g_v^T, 0] (newton_body).  prep layout: ok flag,
+// Ainv (nn x nn), B (nn x nd), F (nn x nd), Sv0 (nd x nd).
+constexpr int kPrepOk = 0;
+__host__ __device__ inline int prep_size(int nn, int nd) {
+  return 1 + nn * nn + 2 * nn * nd + nd * nd;
+}
+
+__global__ void __launch_bounds__(kFitThreads)
+min_prep(const double* __restrict__ R, const double* __restrict__ S, int nn, int nd,
+         double* __restrict__ prep) {
+  extern __shared__ __align__(16) double fsm[];
+  const int n = nn + nd;
+  double* H = fsm;              // n x n (2 H0)
+  double* L = H + n * n;        // nn x nn Cholesky factor
+  __shared__ int ok;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int a = e / n, b = e % n;
+    double h = 0.0;
+    for (int i = 0; i <= (a < b ? a : b); ++i) h = fma(R[i * n + a], R[i * n + b], h);
+    H[e] = 2.0 * S[a] * S[b] * h;
+  }
+  for (int e = threadIdx.x; e < nn * nn; e += blockDim.x) L[e] = 0.0;
+  if (threadIdx.x == 0) ok = 1;
+  __syncthreads();
+  // Cholesky of A = H_uu (left-looking, column j by the block)
+  for (int j = 0; j < nn; ++j) {
+    if (threadIdx.x == 0) {
+      double d = H[j * n + j];
+      for (int k = 0; k < j; ++k) d -= L[j * nn + k] * L[j * nn + k];
+      if (!(d > 0.0) || !isfinite(d)) ok = 0;
+      L[j * nn + j] = ok ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    for (int i = j + 1 + (int)threadIdx.x; i < nn; i += blockDim.x) {
+      double t = H[i * n + j];
+      for (int k = 0; k < j; ++k) t -= L[i * nn + k] * L[j * nn + k];
+      L[i * nn + j] = t / L[j * nn + j];
+    }
+    __syncthreads();
+  }
+  double* Ainv = prep + 1;
+  double* B = Ainv + nn * nn;
+  double* Fm = B + nn * nd;
+  double* Sv0 = Fm + nn * nd;
+  if (threadIdx.x == 0) prep[kPrepOk] = ok ? 1.0 : 0.0;
+  if (!ok) return;
+  // Ainv = (L L^T)^-1, one column per thread (forward then backward solve)
+  for (int col = threadIdx.x; col < nn; col += blockDim.x) {
+    double z[64];
+    for (int i = 0; i < nn; ++i) {
+      double t = i == col ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) t -= L[i * nn + k] * z[k];
+      z[i] = t / L[i * nn + i];
+    }
+    for (int i = nn - 1; i >= 0; --i) {
+      double t = z[i];
+      for (int k = i + 1; k < nn; ++k) t -= L[k * nn + i] * z[k];
+      z[i] = t / L[i * nn + i];
+    }
+    for (int i = 0; i < nn; ++i) Ainv[i * nn + col] = z[i];
+  }
+  for (int e = threadIdx.x; e < nn * nd; e += blockDim.x) B[e] = H[(e / nd) * n + nn + (e % nd)];
+  __syncthreads();
+  for (int e = threadIdx.x; e < nn * nd; e += blockDim.x) {
+    const int i = e / nd, j = e % nd;
+    double t = 0.0;
+    for (int k = 0; k < nn; ++k) t = fma(Ainv[i * nn + k], B[k * nd + j], t);
+    Fm[e] = t;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nd * nd; e += blockDim.x) {
+    const int a = e / nd, b = e % nd;
+    double t = H[(nn + a) * n + nn + b];
+    for (int k = 0; k < nn; ++k) t -= B[k * nd + a] * Fm[k * nd + b];
+    Sv0[e] = t;
+  }
+}
+
 // Newton step: grad = 2 H0 c - mu Q^T(1/q), H = 2 H0 + mu Q^T diag(1/q^2) Q,
 // KKT [H g; g^T 0] [dc; l] = [-grad; 0] solved by Gaussian elimination with
 // partial pivoting (the reference uses LDLT), decrement = -grad.dc,
@@ -872,7 +956,8 @@ __global__ void min_setup(const double* __restrict__ R, const double* __restrict
 __device__ void newton_body(const double* __restrict__ R, const double* __restrict__ S,
                             const double* __restrict__ gsum, const double* __restrict__ pass_out,
                             const double* __restrict__ c, int nn, int nd, double* __restrict__ dc,
-                            const double mu, MinState* __restrict__ st) {
+                            const double mu, MinState* __restrict__ st,
+                            const double* __restrict__ prep = nullptr) {
   extern __shared__ __align__(16) double fsm[];
   const int n = nn + nd, N = n + 1;
   double* K = fsm;                 // N x (N+1) augmented, row-major
@@ -898,6 +983,88 @@ __device__ void newton_body(const double* __restrict__ R, const double* __restri
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     double qterm = k >= nn ? S[k] * gq[k - nn] : 0.0;
     grad[k] = 2.0 * H0c[k] - mu * qterm;
+  }
+  if (prep && prep[kPrepOk] != 0.0 && nd <= 16) {
+    // Schur-complement path (min_prep): t = A^-1 (-grad_u),
+    // [Sv0 + mu M_vv, g_v; g_v^T, 0][dv; l] = [-grad_v - B^T t; 0],
+    // du = t - F dv.
+    const double* Ainv = prep + 1;
+    const double* B = Ainv + nn * nn;
+    const double* Fm = B + nn * nd;
+    const double* Sv0 = Fm + nn * nd;
+    double* tu = K;             // nn
+    double* Ks = tu + nn;       // (nd+1) x (nd+2)
+    const int M = nd + 1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+      double t = 0.0;
+      for (int k = 0; k < nn; ++k) t = fma(Ainv[i * nn + k], -grad[k], t);
+      tu[i] = t;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nd * nd; e += blockDim.x) {
+      const int a = e / nd, b = e % nd;
+      Ks[a * (M + 1) + b] = Sv0[e] + mu * S[nn + a] * S[nn + b] * G[a * nd + b];
+    }
+    for (int a = threadIdx.x; a < nd; a += blockDim.x) {
+      double t = -grad[nn + a];
+      for (int k = 0; k < nn; ++k) t -= B[k * nd + a] * tu[k];
+      const double g = gsum[a] * S[nn + a];
+      Ks[a * (M + 1) + nd] = g;
+      Ks[nd * (M + 1) + a] = g;
+      Ks[a * (M + 1) + M] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Ks[nd * (M + 1) + nd] = 0.0;
+      Ks[nd * (M + 1) + M] = 0.0;
+      // (nd+1)-square Gaussian elimination with partial pivoting
+      bool sing = false;
+      for (int col = 0; col < M; ++col) {
+        int p = col;
+        for (int r = col + 1; r < M; ++r)
+          if (fabs(Ks[r * (M + 1) + col]) > fabs(Ks[p * (M + 1) + col])) p = r;
+        if (Ks[p * (M + 1) + col] == 0.0) sing = true;
+        if (p != col)
+          for (int j = 0; j <= M; ++j) {
+            const double t = Ks[col * (M + 1) + j];
+            Ks[col * (M + 1) + j] = Ks[p * (M + 1) + j];
+            Ks[p * (M + 1) + j] = t;
+          }
+        for (int r = col + 1; r < M; ++r) {
+          const double f = Ks[r * (M + 1) + col] / Ks[col * (M + 1) + col];
+          for (int j = col + 1; j <= M; ++j) Ks[r * (M + 1) + j] -= f * Ks[col * (M + 1) + j];
+        }
+      }
+      for (int r = M - 1; r >= 0; --r) {
+        double t = Ks[r * (M + 1) + M];
+        for (int j = r + 1; j < M; ++j) t -= Ks[r * (M + 1) + j] * Ks[j * (M + 1) + M];
+        Ks[r * (M + 1) + M] = t / Ks[r * (M + 1) + r];  // solution stored in the rhs column
+      }
+      st->ok = sing ? 0 : 1;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+      double t = tu[i];
+      for (int j = 0; j < nd; ++j) t -= Fm[i * nd + j] * Ks[j * (M + 1) + M];
+      dc[i] = t;
+    }
+    for (int j = threadIdx.x; j < nd; j += blockDim.x) dc[nn + j] = Ks[j * (M + 1) + M];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bool finite = st->ok != 0;
+      double dec = 0.0;
+      for (int k = 0; k < n; ++k) {
+        finite &= isfinite(dc[k]);
+        dec = fma(-grad[k], dc[k], dec);
+      }
+      st->ok = finite ? 1 : 0;
+      st->decrement = dec;
+      double a2 = 0.0;
+      for (int i = 0; i < n; ++i) a2 = fma(RSc[i], RSc[i], a2);
+      st->phi0 = a2 - mu * pass_out[1];
+    }
+    return;
   }
   // H entries
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
@@ -1023,7 +1190,8 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
                                               const double* __restrict__ pass_out,
                                               double* __restrict__ c, int nn, int nd,
                                               double* __restrict__ dc, MinCtl* __restrict__ ctl,
-                                              MinState* __restrict__ scratch) {
+                                              MinState* __restrict__ scratch,
+                                              const double* __restrict__ prep) {
   const int ph = ctl->phase;
   if (ph >= kMinDone) return;
   const int n = nn + nd;
@@ -1038,7 +1206,7 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
     R = Rs;
   }
   if (ph == kMinNewton) {
-    newton_body(R, S, gsum, pass_out, c, nn, nd, dc, ctl->mu, scratch);
+    newton_body(R, S, gsum, pass_out, c, nn, nd, dc, ctl->mu, scratch, prep);
     __syncthreads();
     if (threadIdx.x == 0) {
       if (!scratch->ok) {
@@ -1128,7 +1296,7 @@ min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __
          unsigned* __restrict__ counter /* n_groups + 1 */, double* __restrict__ gpart,
          const double* __restrict__ R, const double* __restrict__ S,
          const double* __restrict__ gsum, double* __restrict__ c, double* __restrict__ dc,
-         MinCtl* __restrict__ ctl, MinState* __restrict__ scratch) {
+         MinCtl* __restrict__ ctl, MinState* __restrict__ scratch, const double* __restrict__ prep) {
   if (src.ctl->phase >= kMinDone) return;
   den_pass_body<NDT>(F, nullptr, nullptr, nullptr, 1, 1, partial, src);
   const int W = 2 * kAlphas + F.nd + F.nd * F.nd;
@@ -1156,7 +1324,7 @@ min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __
   const int ph = ctl->phase;
   den_pass_reduce(gpart, n_groups, F.nd, pass_out);
   __syncthreads();
-  ctl_step_body(R, S, gsum, pass_out, c, F.nn, F.nd, dc, ctl, scratch);
+  ctl_step_body(R, S, gsum, pass_out, c, F.nn, F.nd, dc, ctl, scratch, prep);
   __syncthreads();
   if (threadIdx.x == 0) {
     counter[n_groups] = 0u;
@@ -1281,9 +1449,22 @@ std::vector<std::vector<int>> basis(const int32_t* bounds, int nv) {
   return tuples;
 }
 
+// Scratch buffers are stream-ordered allocations on the fit's stream
+// (cudaMallocAsync from the device's pool, kept cached between calls): no
+// device-wide synchronization per buffer, unlike cudaMalloc / cudaFree.
+thread_local cudaStream_t g_fit_stream = nullptr;
+
+cudaError_t fit_malloc(void** p, size_t bytes) {
+  return g_fit_stream ? cudaMallocAsync(p, bytes, g_fit_stream) : cudaMalloc(p, bytes);
+}
+
 struct DevBuf {
   void* p = nullptr;
-  ~DevBuf() { cudaFree(p); }
+  ~DevBuf() {
+    if (!p) return;
+    if (g_fit_stream) cudaFreeAsync(p, g_fit_stream);
+    else cudaFree(p);
+  }
   template <class T>
   T* as() const { return static_cast<T*>(p); }
 };
@@ -1306,7 +1487,7 @@ int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, c
   const int64_t tiles = (F.m + kTile - 1) / kTile;
   int G = (int)std::min<int64_t>(tiles, 4LL * sms);
   if (G < 1) G = 1;
-  FCUDA(cudaMalloc(&Rbuf->p, sizeof(double) * (size_t)G * ncols * ncols));
+  FCUDA(fit_malloc((void**)&Rbuf->p, sizeof(double) * (size_t)G * ncols * ncols));
   const size_t sm1 = tsqr_smem(ncols);
   FCUDA(cudaFuncSetAttribute(tsqr_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
   tsqr_tiles<<<G, kFitThreads, sm1, s>>>(F, Rbuf->as<double>());
@@ -1317,7 +1498,7 @@ int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, c
   // Rbuf and tmp; the root ends in Rbuf.
   int count = G;
   DevBuf tmp;
-  FCUDA(cudaMalloc(&tmp.p, sizeof(double) * (size_t)G * ncols * ncols));
+  FCUDA(fit_malloc((void**)&tmp.p, sizeof(double) * (size_t)G * ncols * ncols));
   double* in = Rbuf->as<double>();
   double* outb = tmp.as<double>();
   while (count > 1) {
@@ -1361,8 +1542,8 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
     }();
     P->G = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)per_sm * sms));
     P->nd = F.nd;
-    FCUDA(cudaMalloc(&P->part.p, sizeof(double) * (size_t)P->G * W));
-    FCUDA(cudaMalloc(&P->out.p, sizeof(double) * W));
+    FCUDA(fit_malloc((void**)&P->part.p, sizeof(double) * (size_t)P->G * W));
+    FCUDA(fit_malloc((void**)&P->out.p, sizeof(double) * W));
   }
   const size_t sm = den_pass_smem(F);
   if (F.nd <= 8) {
@@ -1388,11 +1569,11 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   const int nn = F.nn, nd = F.nd, n = F.n;
   *found = 0;
   DevBuf c, dc, cd, st, fin;
-  FCUDA(cudaMalloc(&c.p, sizeof(double) * n));
-  FCUDA(cudaMalloc(&dc.p, sizeof(double) * n));
-  FCUDA(cudaMalloc(&cd.p, sizeof(double) * nd));
-  FCUDA(cudaMalloc(&st.p, sizeof(MinState)));
-  FCUDA(cudaMalloc(&fin.p, sizeof(int)));
+  FCUDA(fit_malloc((void**)&c.p, sizeof(double) * n));
+  FCUDA(fit_malloc((void**)&dc.p, sizeof(double) * n));
+  FCUDA(fit_malloc((void**)&cd.p, sizeof(double) * nd));
+  FCUDA(fit_malloc((void**)&st.p, sizeof(MinState)));
+  FCUDA(fit_malloc((void**)&fin.p, sizeof(int)));
   Pass P;
   // q of the start vector: Q (start / S) = D start_den.
   FCUDA(cudaMemcpyAsync(cd.p, start + nn, sizeof(double) * nd, cudaMemcpyDeviceToDevice, s));
@@ -1407,7 +1588,7 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   // newton_body's KKT workspace + the staged R (ctl_step_body)
   const size_t smk = sizeof(double) * ((size_t)(n + 1) * (n + 2) + 3 * (size_t)n + (size_t)n * n);
   DevBuf ctlb;
-  FCUDA(cudaMalloc(&ctlb.p, sizeof(MinCtl)));
+  FCUDA(fit_malloc((void**)&ctlb.p, sizeof(MinCtl)));
   MinCtl hc{};
   hc.phase = kMinNewton;
   hc.mu = hs.mu;
@@ -1417,13 +1598,20 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   const int n_groups = (P.G + kStepGroup - 1) / kStepGroup;
   const int Wp = 2 * kAlphas + nd + nd * nd;
   DevBuf counter, gpart;
-  FCUDA(cudaMalloc(&counter.p, sizeof(unsigned) * (n_groups + 1)));
+  FCUDA(fit_malloc((void**)&counter.p, sizeof(unsigned) * (n_groups + 1)));
   FCUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned) * (n_groups + 1), s));
-  FCUDA(cudaMalloc(&gpart.p, sizeof(double) * (size_t)n_groups * Wp));
+  FCUDA(fit_malloc((void**)&gpart.p, sizeof(double) * (size_t)n_groups * Wp));
   const size_t smstep = std::max(smk, den_pass_smem(F));
   FCUDA(cudaFuncSetAttribute(min_step<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smstep));
   FCUDA(cudaFuncSetAttribute(min_step<kMaxCols>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smstep));
+  // Constant-block factorization for the Schur-complement Newton solve.
+  DevBuf prepb;
+  FCUDA(fit_malloc((void**)&prepb.p, sizeof(double) * (size_t)prep_size(nn, nd)));
+  const size_t smp = sizeof(double) * ((size_t)n * n + (size_t)nn * nn);
+  FCUDA(cudaFuncSetAttribute(min_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+  min_prep<<<1, kFitThreads, smp, s>>>(R, S, nn, nd, prepb.as<double>());
+  FCUDA(cudaGetLastError());
   const CtlSrc src{dctl, c.as<double>(), dc.as<double>(), S};
   // Steps (controlled den_pass + reduction + Newton-or-line update) are
   // enqueued in chunks; the host only polls the phase between chunks.
@@ -1435,11 +1623,11 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
         min_step<8><<<P.G, kFitThreads, smstep, s>>>(F, src, P.part.as<double>(), P.out.as<double>(),
                                                      counter.as<unsigned>(), gpart.as<double>(), R, S,
                                                      gsum, c.as<double>(), dc.as<double>(), dctl,
-                                                     st.as<MinState>());
+                                                     st.as<MinState>(), prepb.as<double>());
       else
         min_step<kMaxCols><<<P.G, kFitThreads, smstep, s>>>(
             F, src, P.part.as<double>(), P.out.as<double>(), counter.as<unsigned>(), gpart.as<double>(),
-            R, S, gsum, c.as<double>(), dc.as<double>(), dctl, st.as<MinState>());
+            R, S, gsum, c.as<double>(), dc.as<double>(), dctl, st.as<MinState>(), prepb.as<double>());
     }
     FCUDA(cudaGetLastError());
     FCUDA(cudaMemcpyAsync(&hc, ctlb.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
@@ -1471,7 +1659,7 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
   DevBuf dm;
   FitParams F = F0;
   static const bool use_dm = getenv("RPG_FIT_NO_DM") == nullptr;
-  if (use_dm && cudaMalloc(&dm.p, sizeof(double) * (size_t)F0.m * (nd <= 8 ? 8 : nd)) == cudaSuccess) {
+  if (use_dm && fit_malloc((void**)&dm.p, sizeof(double) * (size_t)F0.m * (nd <= 8 ? 8 : nd)) == cudaSuccess) {
     den_monomials<<<(int)std::min<int64_t>((F0.m + 255) / 256, 8LL * sms), 256, 0, s>>>(
         F0, dm.as<double>());
     FCUDA(cudaGetLastError());
@@ -1482,8 +1670,8 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
   DevBuf gpart, gsum, Rvy, Rv, z, sv, Wv, Uv, dummy, start, refined, next, w, Rw, Sw;
   // column sums of the raw denominator monomials
   const int G = std::max(1, std::min<int>((int)((F.m + 255) / 256), 2 * sms));
-  FCUDA(cudaMalloc(&gpart.p, sizeof(double) * (size_t)G * nd));
-  FCUDA(cudaMalloc(&gsum.p, sizeof(double) * nd));
+  FCUDA(fit_malloc((void**)&gpart.p, sizeof(double) * (size_t)G * nd));
+  FCUDA(fit_malloc((void**)&gsum.p, sizeof(double) * nd));
   const size_t smc = sizeof(double) * kMaxCols * kFitWarps + (size_t)kMaxCols * RPG_MAX_VARS + 16;
   FCUDA(cudaFuncSetAttribute(den_colsum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc));
   den_colsum<<<G, kFitThreads, smc, s>>>(F, gpart.as<double>());
@@ -1494,29 +1682,29 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
   Fv.with_y_col = 1;
   int rc = tsqr(Fv, nn + 1, sms, &Rvy, s, err, errlen);
   if (rc) return rc;
-  FCUDA(cudaMalloc(&Rv.p, sizeof(double) * nn * nn));
-  FCUDA(cudaMalloc(&z.p, sizeof(double) * nn));
+  FCUDA(fit_malloc((void**)&Rv.p, sizeof(double) * nn * nn));
+  FCUDA(fit_malloc((void**)&z.p, sizeof(double) * nn));
   split_vy<<<1, 128, 0, s>>>(Rvy.as<double>(), nn, Rv.as<double>(), z.as<double>());
-  FCUDA(cudaMalloc(&sv.p, sizeof(double) * nn));
-  FCUDA(cudaMalloc(&Wv.p, sizeof(double) * nn * nn));
-  FCUDA(cudaMalloc(&Uv.p, sizeof(double) * nn * nn));
-  FCUDA(cudaMalloc(&dummy.p, sizeof(double) * nn));
+  FCUDA(fit_malloc((void**)&sv.p, sizeof(double) * nn));
+  FCUDA(fit_malloc((void**)&Wv.p, sizeof(double) * nn * nn));
+  FCUDA(fit_malloc((void**)&Uv.p, sizeof(double) * nn * nn));
+  FCUDA(fit_malloc((void**)&dummy.p, sizeof(double) * nn));
   const size_t sm3 = sizeof(double) * (2 * (size_t)kMaxCols * kMaxCols + kMaxCols) + sizeof(int) * (kMaxCols + 4);
   svd_small<<<1, kFitThreads, sm3, s>>>(Rv.as<double>(), nn, sv.as<double>(), Wv.as<double>(),
                                         dummy.as<double>(), Uv.as<double>(), 0);
-  FCUDA(cudaMalloc(&start.p, sizeof(double) * n));
+  FCUDA(fit_malloc((void**)&start.p, sizeof(double) * n));
   start_vector<<<1, 32, 0, s>>>(Wv.as<double>(), Uv.as<double>(), sv.as<double>(), z.as<double>(),
                                 nn, nd, rank_tol, start.as<double>());
-  FCUDA(cudaMalloc(&refined.p, sizeof(double) * n));
-  FCUDA(cudaMalloc(&next.p, sizeof(double) * n));
+  FCUDA(fit_malloc((void**)&refined.p, sizeof(double) * n));
+  FCUDA(fit_malloc((void**)&next.p, sizeof(double) * n));
   int found = 0;
   rc = minimizer(F, R, S, gsum.as<double>(), start.as<double>(), refined.as<double>(), &found, sms,
                  s, err, errlen);
   if (rc) return rc;
-  FCUDA(cudaMalloc(&w.p, sizeof(double) * (size_t)F.m));
-  FCUDA(cudaMalloc(&Sw.p, sizeof(double) * n));
+  FCUDA(fit_malloc((void**)&w.p, sizeof(double) * (size_t)F.m));
+  FCUDA(fit_malloc((void**)&Sw.p, sizeof(double) * n));
   DevBuf cdp;
-  FCUDA(cudaMalloc(&cdp.p, sizeof(double) * nd));
+  FCUDA(fit_malloc((void**)&cdp.p, sizeof(double) * nd));
   Pass P;
   for (int round = 0; found && round < 3; ++round) {
     FCUDA(cudaMemcpyAsync(cdp.p, refined.as<double>() + nn, sizeof(double) * nd,
@@ -1575,18 +1763,35 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
   FCUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   struct StreamGuard {
     cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      g_fit_stream = nullptr;
+      cudaStreamDestroy(s);
+    }
   } sg{s};
+  {
+    // Keep freed scratch cached in the device's default pool between fits.
+    static thread_local int pool_device = -1;
+    if (pool_device != device) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      pool_device = device;
+    }
+  }
+  g_fit_stream = s;
   int sms = 148;
   FCUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   DevBuf dX, dy, dexps, dR, dsig, dV, dscale, dc, dpart, dflags, dstats, dU;
-  FCUDA(cudaMalloc(&dX.p, sizeof(double) * (size_t)m * n_vars));
-  FCUDA(cudaMalloc(&dy.p, sizeof(double) * (size_t)m));
-  FCUDA(cudaMalloc(&dexps.p, exps.size()));
+  FCUDA(fit_malloc((void**)&dX.p, sizeof(double) * (size_t)m * n_vars));
+  FCUDA(fit_malloc((void**)&dy.p, sizeof(double) * (size_t)m));
+  FCUDA(fit_malloc((void**)&dexps.p, exps.size()));
   FCUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * (size_t)m * n_vars, cudaMemcpyHostToDevice, s));
   FCUDA(cudaMemcpyAsync(dy.p, y, sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, s));
   FCUDA(cudaMemcpyAsync(dexps.p, exps.data(), exps.size(), cudaMemcpyHostToDevice, s));
-  FCUDA(cudaMalloc(&dflags.p, sizeof(int) * 8));
+  FCUDA(fit_malloc((void**)&dflags.p, sizeof(int) * 8));
   FCUDA(cudaMemsetAsync(dflags.p, 0, sizeof(int) * 8, s));
 
   FitParams F{};
@@ -1616,10 +1821,10 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
   phase("tsqr");
   // Non-finite entries of A propagate into R (svd, polyfit.hpp:163).
   all_finite<<<1, 256, 0, s>>>(dR.as<double>(), (int64_t)n * n, dflags.as<int>() + 4);
-  FCUDA(cudaMalloc(&dsig.p, sizeof(double) * n));
-  FCUDA(cudaMalloc(&dV.p, sizeof(double) * n * n));
-  FCUDA(cudaMalloc(&dscale.p, sizeof(double) * n));
-  FCUDA(cudaMalloc(&dc.p, sizeof(double) * n));
+  FCUDA(fit_malloc((void**)&dsig.p, sizeof(double) * n));
+  FCUDA(fit_malloc((void**)&dV.p, sizeof(double) * n * n));
+  FCUDA(fit_malloc((void**)&dscale.p, sizeof(double) * n));
+  FCUDA(fit_malloc((void**)&dc.p, sizeof(double) * n));
   const size_t sm3 = sizeof(double) * (2 * (size_t)kMaxCols * kMaxCols + kMaxCols) + sizeof(int) * (kMaxCols + 4);
   FCUDA(cudaFuncSetAttribute(svd_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
   svd_small<<<1, kFitThreads, sm3, s>>>(dR.as<double>(), n, dsig.as<double>(), dV.as<double>(),
@@ -1628,8 +1833,8 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
   smallest_vector<<<1, 64, 0, s>>>(dV.as<double>(), dscale.as<double>(), n, dc.as<double>());
   // Safeguard trigger statistics.
   const int G = std::max(1, std::min<int>((int)((m + 255) / 256), 4 * sms));
-  FCUDA(cudaMalloc(&dpart.p, sizeof(double) * 4 * G));
-  FCUDA(cudaMalloc(&dstats.p, sizeof(double) * 4));
+  FCUDA(fit_malloc((void**)&dpart.p, sizeof(double) * 4 * G));
+  FCUDA(fit_malloc((void**)&dstats.p, sizeof(double) * 4));
   const size_t sm4 = sizeof(double) * 32 + (size_t)kMaxCols * RPG_MAX_VARS + 16;
   den_stats<<<G, 256, sm4, s>>>(F, dc.as<double>() + nn, dpart.as<double>());
   den_stats_final<<<1, 32, 0, s>>>(dpart.as<double>(), G, m, dflags.as<int>() + 0,
