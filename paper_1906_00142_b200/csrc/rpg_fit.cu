@@ -176,30 +176,36 @@ tsqr_tiles(const FitParams F, double* __restrict__ Rout) {
   for (int e = threadIdx.x; e < ncols * ncols; e += blockDim.x) out[e] = R[e];
 }
 
-// K3b: one tree level, Rout[b] <- qr([Rin[2b]; Rin[2b+1]]).R (Rin[2b] alone
-// when 2b+1 is past the level) — ping-pong buffers, no compaction copies.
+// K3b: one tree level of radix kCombine: Rout[b] <- qr([Rin[kb]; Rin[kb+1];
+// ...; Rin[kb+k-1]]).R — the first factor is the running R, the others are
+// stacked as one (k-1) n-row tile (fewer, wider levels: each fold costs n
+// block-synchronised column steps whatever its height).  Ping-pong buffers.
+constexpr int kCombine = 8;
+
 __global__ void __launch_bounds__(kFitThreads)
 tsqr_combine(const double* __restrict__ Rs, int count, int n, double* __restrict__ Rout) {
   extern __shared__ __align__(16) double fsm[];
+  const int first = kCombine * blockIdx.x;
+  const int k = min(kCombine, count - first);  // factors in this group
+  const int rows = (k - 1) * n;
   double* R = fsm;
-  double* T = R + n * n;
-  double* red = T + n * n;
+  double* T = R + n * n;                        // rows x n, column-major (ld = rows)
+  double* red = T + (size_t)(kCombine - 1) * n * n;
   double* wbuf = red + 32;
-  const int a = 2 * blockIdx.x, b = a + 1;
-  const double* Ra = Rs + (size_t)a * n * n;
+  const double* Ra = Rs + (size_t)first * n * n;
   double* out = Rout + (size_t)blockIdx.x * n * n;
-  if (b >= count) {
+  if (k == 1) {
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) out[e] = Ra[e];
     return;
   }
-  const double* Rb = Rs + (size_t)b * n * n;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    R[e] = Ra[e];
-    const int i = e / n, k = e % n;  // Rb row-major -> T column-major (ld = n)
-    T[k * n + i] = Rb[e];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) R[e] = Ra[e];
+  for (int e = threadIdx.x; e < rows * n; e += blockDim.x) {
+    const int f = e / (n * n), w = e % (n * n);  // factor f+1, entry (i, col) row-major
+    const int i = w / n, col = w % n;
+    T[col * rows + f * n + i] = Ra[(size_t)(f + 1) * n * n + w];
   }
   __syncthreads();
-  fold_tile(R, T, n, n, n, red, wbuf);
+  fold_tile(R, T, rows, rows, n, red, wbuf);
   __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) out[e] = R[e];
 }
@@ -1485,14 +1491,17 @@ size_t tsqr_smem(int ncols) {
 int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, char* err,
          size_t errlen) {
   const int64_t tiles = (F.m + kTile - 1) / kTile;
+  const size_t sm1 = tsqr_smem(ncols);
+  int per_sm = 1;
+  FCUDA(cudaFuncSetAttribute(tsqr_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+  FCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_tiles, kFitThreads, sm1));
+  (void)per_sm;
   int G = (int)std::min<int64_t>(tiles, 4LL * sms);
   if (G < 1) G = 1;
   FCUDA(fit_malloc((void**)&Rbuf->p, sizeof(double) * (size_t)G * ncols * ncols));
-  const size_t sm1 = tsqr_smem(ncols);
-  FCUDA(cudaFuncSetAttribute(tsqr_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
   tsqr_tiles<<<G, kFitThreads, sm1, s>>>(F, Rbuf->as<double>());
   FCUDA(cudaGetLastError());
-  const size_t sm2 = sizeof(double) * (2 * (size_t)ncols * ncols + 32 + kMaxCols);
+  const size_t sm2 = sizeof(double) * ((size_t)kCombine * ncols * ncols + 32 + kMaxCols);
   FCUDA(cudaFuncSetAttribute(tsqr_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
   // Tree over the G factors, one launch per level, ping-ponging between
   // Rbuf and tmp; the root ends in Rbuf.
@@ -1502,7 +1511,7 @@ int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, c
   double* in = Rbuf->as<double>();
   double* outb = tmp.as<double>();
   while (count > 1) {
-    const int next = (count + 1) / 2;
+    const int next = (count + kCombine - 1) / kCombine;
     tsqr_combine<<<next, kFitThreads, sm2, s>>>(in, count, ncols, outb);
     FCUDA(cudaGetLastError());
     std::swap(in, outb);
