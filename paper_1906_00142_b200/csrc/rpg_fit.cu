@@ -221,7 +221,7 @@ __device__ void jacobi_svd(double* M, double* V, int n, int* rot_flag) {
     if (threadIdx.x == 0) *rot_flag = 0;
     __syncthreads();
     for (int step = 0; step < np - 1; ++step) {
-      for (int pr = warp; pr < np / 2; pr += kFitWarps) {
+      for (int pr = warp; pr < np / 2; pr += (int)(blockDim.x >> 5)) {
         // round-robin pairing: slot 0 fixed, others rotate
         int a = pr == 0 ? 0 : 1 + (pr - 1 + step) % (np - 1);
         int b = 1 + (np - 2 - pr + step) % (np - 1);
@@ -263,7 +263,13 @@ __device__ void jacobi_svd(double* M, double* V, int n, int* rot_flag) {
 // K3c: one CTA.  In: R (n x n row-major).  Out: sigma (n, descending),
 // Vs (n x n column-major, columns = right singular vectors of A S, sorted),
 // col_scale (n), c (n) = V[:, n-1] .* col_scale.
-__global__ void __launch_bounds__(kFitThreads)
+// Threads of svd_small: one warp per rotation pair of a round-robin step.
+__host__ __device__ inline int svd_threads(int n) {
+  const int pairs = ((n + 1) & ~1) / 2;
+  return 32 * (pairs < 8 ? 8 : pairs > 32 ? 32 : pairs);
+}
+
+__global__ void __launch_bounds__(1024)
 svd_small(const double* __restrict__ R, int n, double* __restrict__ sigma,
           double* __restrict__ Vout, double* __restrict__ col_scale,
           double* __restrict__ Uout, int equilibrate) {
@@ -1699,7 +1705,7 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
   FCUDA(fit_malloc((void**)&Uv.p, sizeof(double) * nn * nn));
   FCUDA(fit_malloc((void**)&dummy.p, sizeof(double) * nn));
   const size_t sm3 = sizeof(double) * (2 * (size_t)kMaxCols * kMaxCols + kMaxCols) + sizeof(int) * (kMaxCols + 4);
-  svd_small<<<1, kFitThreads, sm3, s>>>(Rv.as<double>(), nn, sv.as<double>(), Wv.as<double>(),
+  svd_small<<<1, svd_threads(nn), sm3, s>>>(Rv.as<double>(), nn, sv.as<double>(), Wv.as<double>(),
                                         dummy.as<double>(), Uv.as<double>(), 0);
   FCUDA(fit_malloc((void**)&start.p, sizeof(double) * n));
   start_vector<<<1, 32, 0, s>>>(Wv.as<double>(), Uv.as<double>(), sv.as<double>(), z.as<double>(),
@@ -1836,7 +1842,7 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
   FCUDA(fit_malloc((void**)&dc.p, sizeof(double) * n));
   const size_t sm3 = sizeof(double) * (2 * (size_t)kMaxCols * kMaxCols + kMaxCols) + sizeof(int) * (kMaxCols + 4);
   FCUDA(cudaFuncSetAttribute(svd_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
-  svd_small<<<1, kFitThreads, sm3, s>>>(dR.as<double>(), n, dsig.as<double>(), dV.as<double>(),
+  svd_small<<<1, svd_threads(n), sm3, s>>>(dR.as<double>(), n, dsig.as<double>(), dV.as<double>(),
                                         dscale.as<double>(), nullptr, 1);
   FCUDA(cudaGetLastError());
   smallest_vector<<<1, 64, 0, s>>>(dV.as<double>(), dscale.as<double>(), n, dc.as<double>());
