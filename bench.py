@@ -12,6 +12,9 @@ per GPU.  Multi-GPU: rank r sweeps the next 65,473 N values (weak scaling
 along the data-parameter axis) and the per-N winner records are all-gathered
 over NCCL inside the timed region.
 
+`--workload c4` times the parameter-estimation fit (configs[3]: 5 metrics x
+10^6 samples; samples/s; CPU baseline = O3 on a bounded sample) and
+`--workload dump` the Ec-table dump (GB/s).
 `--workload c3` sweeps the full 27-kernel PolyBench-GPU suite (configs[2]:
 N = 64..65,536 split over the GPUs, strong scaling) and `--workload c5` the
 5-variable stress model over a 182 x 182 (N, M) grid x 30,343 3-D blocks
@@ -433,6 +436,130 @@ def gpu_arm(args):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# C4: the parameter-estimation fit (BASELINE.json configs[3])
+
+C4_SAMPLES = 1_000_000
+C4_CPU_SAMPLES = 20_000     # bounded sample for the O3 CPU legs
+
+
+def c4_data(m: int, noise: float = 0.01, seed: int = 1906):
+    """Synthetic profiled samples: D1 uniform over [64, 65536], (bx, by)
+    uniform over the 7,262 integer configs, y = the GEMM ground truth x
+    (1 + U(-noise, noise)) per metric.  numpy, seeded."""
+    from paper_1906_00142_b200 import formats as F
+    rng = np.random.default_rng(seed)
+    D = rng.integers(64, 65537, m).astype(float)
+    cfg = np.array(F.integer_configs(), dtype=float)[rng.integers(0, 7262, m)][:, :2]
+    X = np.ascontiguousarray(np.column_stack([D, cfg]))
+    spec = F.load_kernel_spec(os.path.join(ROOT, "data", "polybench", "gemm.kernel.json"))
+
+    def poly(p):
+        out = np.zeros(m)
+        for mono, c in zip(p.basis, p.coeffs):
+            if c != 0.0:
+                out += c * np.prod(X ** np.asarray(mono, dtype=float), axis=1)
+        return out
+
+    ys = {}
+    for name in F.REQUIRED_METRICS:
+        f = spec.ground_truth[name]
+        y = poly(f.num) / poly(f.den)
+        if noise > 0:
+            y = y * (1 + rng.uniform(-noise, noise, m))
+        ys[name] = np.ascontiguousarray(y)
+    return X, ys, spec.variables
+
+
+def c4_cpu(threads: int, m: int = C4_CPU_SAMPLES):
+    """O3 (numpy/LAPACK restatement of fit_rational) on a bounded sample."""
+    from oracle import o3_fit as O3
+    X, ys, var = c4_data(m)
+    t0 = time.perf_counter()
+    for y in ys.values():
+        try:
+            O3.fit_rational(X, y, var, [2, 2, 2], [1, 1, 1])
+        except O3.DegenerateFit:
+            pass
+    dt = time.perf_counter() - t0
+    return len(ys) * m / dt, dt, m
+
+
+def c4_arm(args):
+    from paper_1906_00142_b200 import fit as G
+    X, ys, var = c4_data(C4_SAMPLES)
+    nb, db = [2, 2, 2], [1, 1, 1]
+    for _ in range(max(1, args.warmup)):
+        for y in ys.values():
+            try:
+                G.fit_rational(X, y, var, nb, db)
+            except (G.DegenerateFit, G.SvdFailure):
+                pass
+    times = []
+    with ClockSampler(0) as clocks:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            for y in ys.values():
+                try:
+                    G.fit_rational(X, y, var, nb, db)
+                except (G.DegenerateFit, G.SvdFailure):
+                    pass
+            times.append(time.perf_counter() - t0)
+    step = statistics.median(times)
+    samples = len(ys) * C4_SAMPLES
+    n = 35
+    qr_flops = len(ys) * (2 * C4_SAMPLES * n * n - 2 * n ** 3 / 3 + 3 * C4_SAMPLES * n)
+    peak_tf, peak_src = fp64_peak_tflops()
+    cpu = None
+    if not args.no_cpu:
+        threads = host_threads()
+        rate, dt, m = c4_cpu(threads)
+        cpu = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "port",
+               "sample": f"O3 (numpy/LAPACK fit_rational restatement), 5 metrics x {m} samples ({dt:.1f} s)"}
+    print(json.dumps({
+        "metric": "C4 rational-fit throughput (samples fitted per second)", "value": samples / step,
+        "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C4: 5 GEMM metrics x 10^6 samples each, variables (D1,bx,by), bounds num "
+                               "(2,2,2) / den (1,1,1) -> 10^6 x 35 sample matrices, 1% uniform noise "
+                               "(positivity safeguard active)", "id": "c4",
+                   "api": "rpg_fit_rational (host buffers, H2D inside the step)"},
+        "roofline": {"bound": "fp64", "achieved": qr_flops / step / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": qr_flops / step / 1e12 / peak_tf, "traffic": None,
+                     "note": "QR-equivalent FLOPs (2mn^2 - 2n^3/3 + 3mn per metric); the positivity "
+                             "minimizer's sample passes are extra work not counted", "peak_source": peak_src},
+        "e2e": {"value": samples / step, "unit": "samples/s",
+                "h2d_bytes_per_step": int(len(ys) * (X.nbytes + C4_SAMPLES * 8)),
+                "d2h_bytes_per_step": len(ys) * n * 8},
+        "cpu_baseline": cpu, "clocks": clocks.summary()}), flush=True)
+    return 0
+
+
+def c4_reference_arm(args):
+    """The reference's fit path (O3 port: numpy/LAPACK) on a bounded sample."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    threads = host_threads()
+    c4_cpu(threads, 2000)  # warm-up
+    times, rate = [], 0.0
+    for _ in range(args.steps):
+        rate, dt, m = c4_cpu(threads)
+        times.append(dt)
+    value = 5 * C4_CPU_SAMPLES * args.steps / sum(times)
+    sample = f"O3 fit_rational, 5 metrics x {C4_CPU_SAMPLES} samples per step"
+    print(json.dumps({
+        "metric": "C4 rational-fit throughput (samples fitted per second)", "value": value,
+        "unit": "samples/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": "C4 (bounded CPU sample)", "id": "c4"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+        flush=True)
+    return 0
+
+
 def dump_arm(args):
     """Ec-table dump (BASELINE.md §3 last row): rpg_evaluate_device writes the
     full per-point table — f64 Ec + u8 case tag + i32 occupancy warps, 13 B per
@@ -495,7 +622,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c2", "c3", "c5", "dump"], default="c2",
+    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5", "dump"], default="c2",
                     help="BASELINE.json config: c2 (default, configs[1]), c3 (full suite), c5 (stress)")
     ap.add_argument("--arith", choices=["exact", "fast"], default="fast")
     ap.add_argument("--kernel", choices=["specialized", "generic"], default="specialized")
@@ -506,11 +633,15 @@ def main():
                     help="test mode: all ranks on cuda:0 (with --dist-backend gloo)")
     args = ap.parse_args()
     if args.impl == "reference":
+        if args.workload == "c4":
+            return c4_reference_arm(args)
         if args.workload == "dump":
             args.workload = "c2"
         return reference_arm(args)
     if args.workload == "dump":
         return dump_arm(args)
+    if args.workload == "c4":
+        return c4_arm(args)
     return gpu_arm(args)
 
 

@@ -64,3 +64,14 @@ def test_reference_arm_line():
     assert d["impl"] == "reference" and d["unit"] == "evals/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_c4_data_shapes_and_reference_arm():
+    X, ys, var = bench.c4_data(1000)
+    assert X.shape == (1000, 3) and var == ["D1", "bx", "by"] and len(ys) == 5
+    assert all(np.isfinite(y).all() and y.shape == (1000,) for y in ys.values())
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "c4",
+                        "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["unit"] == "samples/s" and d["value"] > 0
