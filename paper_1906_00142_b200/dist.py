@@ -10,10 +10,19 @@ One process per GPU (``torch.distributed``; NCCL on GPUs, gloo for CPU
 tests).  ``search_fn`` evaluates one shard and returns its winner records
 (``abi.WINNER_DTYPE``); on a GPU it is ``Plan.search_batch`` (host buffers)
 or a device-buffer variant.
+
+The fit (``fit_all_metrics``, pipeline.hpp:145-184) shards by metric: every
+metric column is an independent least-squares problem over the same samples,
+so each rank fits a contiguous block of the name-sorted metrics and one
+all-gather of the (small) fitted models assembles the same MetricModelSet on
+every rank.  Row-sharding one metric's samples would need a
+collective inside every positivity-minimizer iteration (its line search and
+barrier sums run over all samples), for a fit that already takes ~20 ms per
+10^6-sample metric on one B200; see DESIGN.md §7.
 """
 from __future__ import annotations
 
-from typing import Callable, Tuple
+from typing import Callable, Dict, List, Sequence, Tuple
 
 import numpy as np
 
@@ -58,3 +67,32 @@ def sharded_search(data: np.ndarray, search_fn: Callable[[np.ndarray], np.ndarra
         a, b = shard_range(n, world, r)
         parts.append(allrec[r, : (b - a) * rec])
     return np.concatenate(parts).view(A.WINNER_DTYPE)
+
+
+def sharded_fit_all_metrics(X, metric_values: Dict[str, np.ndarray], variables: Sequence[str],
+                            bounds: Dict[str, Tuple[List[int], List[int]]], constants: Dict[str, float],
+                            rank_tol: float = None, device: int = 0, fit_fn=None, group=None):
+    """pipe::fit_all_metrics (pipeline.hpp:145-184) over the ranks of
+    ``group``: rank r fits the metrics in block shard_range(#metrics, world,
+    r) of the name-sorted list (``fit_fn``: fit.fit_rational on the GPU by
+    default; tests pass oracle O3), then the per-metric outcomes are
+    all-gathered.  Every rank returns the MetricModelSet a single-process
+    fit_all_metrics returns (same models, reports and failures; a total
+    wipeout raises AllMetricsFailed on every rank)."""
+    import torch.distributed as dist
+
+    from . import fit as G
+
+    if rank_tol is None:
+        rank_tol = G.K_DEFAULT_RANK_TOL
+    order = G.check_metric_inputs(X, metric_values, variables, bounds, constants)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi = shard_range(len(order), world, rank)
+    local = G.fit_metrics(X, metric_values, variables, bounds, order[lo:hi], rank_tol, device, fit_fn)
+    gathered: List[dict] = [None] * world
+    dist.all_gather_object(gathered, local, group=group)
+    outcomes: Dict[str, object] = {}
+    for part in gathered:
+        outcomes.update(part)
+    return G.assemble_model_set(variables, constants, outcomes)

@@ -87,17 +87,17 @@ def default_bounds(n_variables: int) -> Tuple[List[int], List[int]]:
     return [2] * n_variables, [1] * n_variables
 
 
-def fit_all_metrics(X, metric_values: Dict[str, np.ndarray], variables: Sequence[str],
-                    bounds: Dict[str, Tuple[List[int], List[int]]],
-                    constants: Dict[str, float], rank_tol: float = K_DEFAULT_RANK_TOL,
-                    device: int = 0) -> F.MetricModelSet:
-    """pipe::fit_all_metrics (pipeline.hpp:145-184): one fit per metric
-    column; numerical failures are recorded per metric, a total wipeout
-    raises AllMetricsFailed."""
+def check_metric_inputs(X, metric_values: Dict[str, np.ndarray], variables: Sequence[str],
+                        bounds: Dict[str, Tuple[List[int], List[int]]],
+                        constants: Dict[str, float]) -> List[str]:
+    """The argument checks of pipe::fit_all_metrics (pipeline.hpp:145-184),
+    all done before any fit runs (a sharded caller runs them on every rank, so
+    a bad argument raises everywhere before any collective).  Returns the
+    metrics in fit order (sorted by name)."""
     if len(X) == 0:
         raise ValueError("fit_all_metrics: sample set is empty")
-    out = F.MetricModelSet(list(variables), {}, {}, dict(constants), {})
-    for metric in sorted(metric_values):
+    order = sorted(metric_values)
+    for metric in order:
         if metric in constants:
             raise F.PipelineError(
                 f"metric '{metric}' is both a sample column and a declared constant")
@@ -105,16 +105,54 @@ def fit_all_metrics(X, metric_values: Dict[str, np.ndarray], variables: Sequence
         if len(nb) != len(variables) or len(db) != len(variables):
             raise F.PipelineError(f"degree bounds for metric '{metric}' must have "
                                   f"{len(variables)} entries per side")
+    return order
+
+
+def fit_metrics(X, metric_values: Dict[str, np.ndarray], variables: Sequence[str],
+                bounds: Dict[str, Tuple[List[int], List[int]]], metrics: Sequence[str],
+                rank_tol: float = K_DEFAULT_RANK_TOL, device: int = 0, fit_fn=None) -> Dict[str, object]:
+    """Fits the listed metrics; per metric the outcome is (RationalFunction,
+    report dict) or, for a numerical failure (``fit_fn`` raised DegenerateFit
+    or SvdFailure), the failure message (str)."""
+    fit_fn = fit_fn or (lambda X_, y_, v_, nb_, db_, tol_: fit_rational(X_, y_, v_, nb_, db_, tol_, device))
+    out: Dict[str, object] = {}
+    for metric in metrics:
+        nb, db = bounds.get(metric, default_bounds(len(variables)))
         try:
-            f, rep = fit_rational(X, metric_values[metric], variables, nb, db, rank_tol, device)
-            out.models[metric] = f
-            out.reports[metric] = {"residual_norm": rep.residual_norm,
-                                   "numerical_rank": rep.numerical_rank,
-                                   "truncated": rep.truncated,
-                                   "singular_values": rep.singular_values}
+            f, rep = fit_fn(X, metric_values[metric], variables, nb, db, rank_tol)
+            out[metric] = (f, {"residual_norm": rep.residual_norm,
+                               "numerical_rank": rep.numerical_rank,
+                               "truncated": rep.truncated,
+                               "singular_values": list(rep.singular_values)})
         except (DegenerateFit, SvdFailure) as e:
-            out.failures[metric] = str(e)
+            out[metric] = str(e)
+    return out
+
+
+def assemble_model_set(variables: Sequence[str], constants: Dict[str, float],
+                       outcomes: Dict[str, object]) -> F.MetricModelSet:
+    """Collects per-metric outcomes into a MetricModelSet in metric-name order;
+    a total wipeout raises AllMetricsFailed (pipeline.hpp:178-183)."""
+    out = F.MetricModelSet(list(variables), {}, {}, dict(constants), {})
+    for metric in sorted(outcomes):
+        o = outcomes[metric]
+        if isinstance(o, str):
+            out.failures[metric] = o
+        else:
+            out.models[metric], out.reports[metric] = o
     if not out.models:
         raise AllMetricsFailed("no metric could be fitted:" +
                                "".join(f" [{k}: {v}]" for k, v in sorted(out.failures.items())))
     return out
+
+
+def fit_all_metrics(X, metric_values: Dict[str, np.ndarray], variables: Sequence[str],
+                    bounds: Dict[str, Tuple[List[int], List[int]]],
+                    constants: Dict[str, float], rank_tol: float = K_DEFAULT_RANK_TOL,
+                    device: int = 0) -> F.MetricModelSet:
+    """pipe::fit_all_metrics (pipeline.hpp:145-184): one fit per metric
+    column; numerical failures are recorded per metric, a total wipeout
+    raises AllMetricsFailed."""
+    order = check_metric_inputs(X, metric_values, variables, bounds, constants)
+    return assemble_model_set(variables, constants,
+                              fit_metrics(X, metric_values, variables, bounds, order, rank_tol, device))

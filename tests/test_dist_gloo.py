@@ -68,3 +68,91 @@ def test_two_rank_gloo_sharded_search_matches_single_process(tmp_path):
     for r in range(2):
         got = np.load(tmp_path / f"rank{r}.npy")
         assert np.array_equal(got, want)
+
+
+# --- metric-sharded fit (pipeline.hpp:145-184 over ranks) -------------------
+
+SENTINEL = -1234.5  # y[0] == SENTINEL makes the test fit_fn fail that metric
+
+
+def _fit_case():
+    from paper_1906_00142_b200 import formats as F
+
+    from .test_oracle_fit import stencil_samples
+    from oracle import o3_fit as O3
+    spec, pts = stencil_samples([64, 128, 256])
+    bounds = {F.METRIC_COMP: ([1, 1, 0], [0, 1, 0]), F.METRIC_UNCOAL: ([0, 1, 0], [0, 1, 0]),
+              F.METRIC_COAL: ([0, 0, 0], [0, 0, 0]), F.METRIC_SYNCH: ([1, 0, 0], [0, 1, 0]),
+              F.METRIC_TOTAL_BLOCKS: ([2, 0, 0], [0, 1, 1])}
+    values = {name: O3.eval_ratfunc(spec.ground_truth[name], pts) for name in bounds}
+    values["zz_failing"] = np.full(len(pts), SENTINEL)
+    return spec, pts, values, bounds, {F.METRIC_REGS: 20.0, F.METRIC_SHARED: 0.0}
+
+
+def _o3_fit(X, y, variables, nb, db, tol):
+    from oracle import o3_fit as O3
+    from paper_1906_00142_b200 import fit as G
+    if y[0] == SENTINEL:
+        raise G.DegenerateFit("test: forced failure")
+    return O3.fit_rational(X, y, variables, nb, db, tol)
+
+
+def _canon(x):
+    """Plain, bit-exact form (floats as hex) of a model set's contents."""
+    if isinstance(x, (float, np.floating)):
+        return float(x).hex()
+    if isinstance(x, (bool, int, str, np.integer)) or x is None:
+        return repr(x)
+    if isinstance(x, dict):
+        return "{" + ",".join(f"{k!r}:{_canon(v)}" for k, v in sorted(x.items())) + "}"
+    if isinstance(x, (list, tuple, np.ndarray)):
+        return "[" + ",".join(_canon(v) for v in x) + "]"
+    return type(x).__name__ + _canon(vars(x))
+
+
+def _model_set_bytes(ms):
+    return _canon(ms).encode()
+
+
+def _fit_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec, pts, values, bounds, consts = _fit_case()
+        ms = D.sharded_fit_all_metrics(pts, values, spec.variables, bounds, consts, fit_fn=_o3_fit)
+        with open(os.path.join(outdir, f"fit{rank}.pkl"), "wb") as f:
+            f.write(_model_set_bytes(ms))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_metric_sharded_fit_matches_single_process(tmp_path, world):
+    from paper_1906_00142_b200 import fit as G
+    port = _free_port()
+    mp.start_processes(_fit_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    spec, pts, values, bounds, consts = _fit_case()
+    order = G.check_metric_inputs(pts, values, spec.variables, bounds, consts)
+    single = G.assemble_model_set(spec.variables, consts,
+                                  G.fit_metrics(pts, values, spec.variables, bounds, order, fit_fn=_o3_fit))
+    assert len(single.models) == 5 and list(single.failures) == ["zz_failing"]
+    want = _model_set_bytes(single)
+    for r in range(world):
+        assert (tmp_path / f"fit{r}.pkl").read_bytes() == want
+
+
+def test_fit_input_checks_run_before_any_fit():
+    from paper_1906_00142_b200 import fit as G
+    from paper_1906_00142_b200 import formats as F
+    spec, pts, values, bounds, consts = _fit_case()
+    with pytest.raises(F.PipelineError):
+        G.check_metric_inputs(pts, values, spec.variables, bounds, {**consts, "zz_failing": 1.0})
+    with pytest.raises(F.PipelineError):
+        G.check_metric_inputs(pts, values, spec.variables, {**bounds, "zz_failing": ([1], [1])}, consts)
+    with pytest.raises(ValueError):
+        G.check_metric_inputs(pts[:0], values, spec.variables, bounds, consts)
+    with pytest.raises(G.AllMetricsFailed):
+        G.assemble_model_set(spec.variables, consts, {"a": "x", "b": "y"})

@@ -95,3 +95,54 @@ def test_bench_two_rank_strong_scaling_line():
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
     assert d["config"]["evals_job_step"] == 182 * 182 * 30343
     assert d["agreement_device_vs_host_api"] is True
+
+
+def _fit_worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+
+    from .test_dist_gloo import _fit_case, _model_set_bytes
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec, pts, values, bounds, consts = _fit_case()
+        values.pop("zz_failing")
+        ms = D.sharded_fit_all_metrics(pts, values, spec.variables, bounds, consts)
+        with open(os.path.join(outdir, f"fit{rank}.txt"), "wb") as f:
+            f.write(_model_set_bytes(ms))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_metric_sharded_gpu_fit_equals_single_process(tmp_path):
+    """dist.sharded_fit_all_metrics with the GPU fit (2 ranks on cuda:0):
+    every rank assembles the MetricModelSet a single-process GPU
+    fit_all_metrics returns, bit for bit (the K3 fit is deterministic)."""
+    from paper_1906_00142_b200 import fit as G
+
+    from .test_dist_gloo import _fit_case, _model_set_bytes
+    port = _free_port()
+    mp.start_processes(_fit_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    spec, pts, values, bounds, consts = _fit_case()
+    values.pop("zz_failing")
+    want = _model_set_bytes(G.fit_all_metrics(pts, values, spec.variables, bounds, consts))
+    for r in range(2):
+        assert (tmp_path / f"fit{r}.txt").read_bytes() == want
+
+
+def test_bench_c4_two_rank_line():
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "1", "--warmup", "3", "--workload", "c4", "--no-cpu",
+           "--dist-backend", "gloo", "--same-device"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["unit"] == "samples/s"
+    assert len(d["config"]["fitted"]) + len(d["config"]["failed"]) == 5 and d["config"]["fitted"]
