@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Dump a bench model's specialized kernel source and compile it with nvcc
 (-Xptxas -v) for register / SASS inspection.  Usage:
-  jit_sass.py [gemm|2dconv|atax1] [fast|exact] [min_blocks]"""
+  jit_sass.py [gemm|2dconv|atax1] [fast|exact] [min_blocks] [threads]
+(defaults: the JIT's — FAST 32 threads x 24 blocks, EXACT 256 x 3)"""
 import ctypes as C
 import os
 import shutil
@@ -14,7 +15,8 @@ from paper_1906_00142_b200 import abi as A, formats as F  # noqa: E402
 
 kern = sys.argv[1] if len(sys.argv) > 1 else "gemm"
 mode = sys.argv[2] if len(sys.argv) > 2 else "fast"
-mb = sys.argv[3] if len(sys.argv) > 3 else "3"
+th = sys.argv[4] if len(sys.argv) > 4 else ("32" if mode == "fast" else "256")
+mb = sys.argv[3] if len(sys.argv) > 3 else str(768 // int(th))
 out = "/tmp/rpg_jit_sass"
 os.makedirs(out, exist_ok=True)
 lib = A.load_library()
@@ -33,7 +35,7 @@ for h in ("paper_1906_00142_b200/csrc/rpg_device.cuh", "paper_1906_00142_b200/cs
     shutil.copy(os.path.join(ROOT, h), out)
 cubin = src.replace(".cu", f"_{mb}.cubin")
 r = subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-fmad=false",
-                    f"-DRPG_MIN_BLOCKS={mb}", "-cubin", "-Xptxas", "-v", "-o", cubin, src],
+                    f"-DRPG_MIN_BLOCKS={mb}", f"-DRPG_THREADS={th}", "-cubin", "-Xptxas", "-v", "-o", cubin, src],
                    capture_output=True, text=True)
 print("\n".join(l for l in r.stderr.splitlines() if "registers" in l or "spill" in l or "error" in l))
 print(cubin)
