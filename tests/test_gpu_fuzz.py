@@ -69,3 +69,43 @@ def test_fuzz_bit_exact(seed, arith, kernel):
     assert np.array_equal(tag, otag)
     assert np.array_equal(wocc, owocc)
     assert np.array_equal(win.view(np.uint8), owin.view(np.uint8)), (win, owin)
+
+
+def _edge_case(seed):
+    """Metric magnitudes around the specialized kernel's quotient range
+    tests (rpg_device.cuh ratio_fast / FastDiv): numerators near 2^-969 and
+    2^-928 (tiny dividend, tiny quotient), denominators near 2^-39, quotients
+    near 2^38, plus plain ones — each metric picks one regime at random."""
+    rng = np.random.default_rng(5000 + seed)
+    variables = ["D1", "bx", "by"]
+    spec = zoo.random_spec(rng, variables, positive=True, sparsity=0.3)
+    regimes = [(-969, 0), (-928, 0), (-931, -39), (0, -39), (0, -41), (38, 0), (36, -3), (0, 0)]
+    for f in spec.models.values():
+        en, ed = regimes[int(rng.integers(len(regimes)))]
+        en += int(rng.integers(-3, 4))
+        ed += int(rng.integers(-3, 4))
+        f.num.coeffs = [c * 2.0 ** en for c in f.num.coeffs]
+        f.den.coeffs = [c * 2.0 ** ed for c in f.den.coeffs]
+    hw = zoo.random_hw(rng)
+    full = F.integer_configs(1024, dims=2)
+    idx = np.sort(rng.choice(len(full), size=int(rng.integers(200, 900)), replace=False))
+    data = rng.integers(1, 70000, size=(int(rng.integers(3, 9)), 1)).astype(np.int64)
+    return spec, hw, [full[i] for i in idx], data, "real"
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_division_edges_bit_exact(seed, arith):
+    spec, hw, space, data, rep = _edge_case(seed)
+    opts = _opts(arith, "specialized", rep)
+    pk = A.PackedModel(spec, drop_zero_terms=False)
+    args = (pk, A.profile_struct(hw), opts.struct(), A.config_array(space), data)
+    oec, otag, owocc = o1.evaluate_batch(*args, 4)
+    owin = o1.search_batch(*args, 4)
+    with S.Plan(spec, hw, space, opts) as plan:
+        ec, tag, wocc = plan.evaluate(data)
+        win = plan.search_batch(data)
+    assert np.array_equal(ec.view(np.int64), oec.view(np.int64))
+    assert np.array_equal(tag, otag)
+    assert np.array_equal(wocc, owocc)
+    assert np.array_equal(win.view(np.uint8), owin.view(np.uint8)), (win, owin)
