@@ -124,6 +124,21 @@ def official_flops(spec) -> int:
     return total
 
 
+def count_kernel_launches(fn, prefix="rpg_"):
+    """Kernels whose name starts with `prefix` that one call of fn launches,
+    counted by the CUDA activity trace (torch.profiler / CUPTI) outside the
+    timed region; None if tracing is unavailable."""
+    try:
+        import torch
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        return sum(1 for e in prof.events() if e.device_type.name == "CUDA" and e.name.startswith(prefix))
+    except Exception:  # noqa: BLE001 - diagnostics only
+        return None
+
+
 def fp64_peak_tflops():
     """Measured FP64 (DFMA) peak: live run of tools/fp64_peak when built,
     else the committed measurement."""
@@ -534,6 +549,7 @@ def c4_arm(args):
             t = t.cuda()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_s = float(t.cpu()[0])
+    per_step = count_kernel_launches(step) if world == 1 else None  # (a collective step cannot run on one rank)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -567,6 +583,8 @@ def c4_arm(args):
         "e2e": {"value": samples / step_s, "unit": "samples/s",
                 "h2d_bytes_per_step": int(len(ys) * (X.nbytes + C4_SAMPLES * 8)),
                 "d2h_bytes_per_step": len(ys) * n * 8},
+        "gpu_launches": per_step * args.steps if per_step is not None else None,
+        "gpu_launches_note": "rank 0's rpg_* kernels per step (CUDA activity trace of one extra untimed step) x steps",
         "cpu_baseline": cpu, "clocks": clocks.summary()}), flush=True)
     if world > 1:
         dist.destroy_process_group()
