@@ -679,7 +679,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5", "dump"], default="c2",
                     help="BASELINE.json config: c2 (default, configs[1]), c3 (full suite), c5 (stress)")
-    ap.add_argument("--arith", choices=["exact", "fast"], default="fast")
+    ap.add_argument("--arith", choices=["exact", "fast", "fastcm"], default=None,
+                    help="default: fastcm (configuration-major) for the one-data-parameter C2/C3 "
+                         "searches, fast otherwise (C5's two data parameters, the Ec dump)")
     ap.add_argument("--kernel", choices=["specialized", "generic"], default="specialized")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -687,6 +689,8 @@ def main():
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: all ranks on cuda:0 (with --dist-backend gloo)")
     args = ap.parse_args()
+    if args.arith is None:
+        args.arith = "fastcm" if args.workload in ("c2", "c3") and args.kernel == "specialized" else "fast"
     if args.impl == "reference":
         if args.workload == "c4":
             return c4_reference_arm(args)

@@ -87,8 +87,14 @@ enum { RPG_REP_REAL = 0, RPG_REP_CEIL = 1 };
  *                    contraction — bit-identical to oracle O1.
  *   RPG_ARITH_FAST:  per-data-tuple collapse of the data-parameter part of
  *                    every polynomial and DFMA Horner evaluation of the
- *                    block-dimension part (bit-identical to O1's FAST twin). */
-enum { RPG_ARITH_EXACT = 0, RPG_ARITH_FAST = 1 };
+ *                    block-dimension part (bit-identical to O1's FAST twin).
+ *   RPG_ARITH_FAST_CM: the dual order — per-configuration collapse of the
+ *                    block-dimension part (fma in basis order, once per
+ *                    plan) and DFMA Horner in the data parameter per point
+ *                    (bit-identical to O1's FAST_CM twin).  Searches only
+ *                    (rpg_search_batch / _device); models with one data
+ *                    parameter whose regs/shared metrics are constants. */
+enum { RPG_ARITH_EXACT = 0, RPG_ARITH_FAST = 1, RPG_ARITH_FAST_CM = 2 };
 
 enum {
   RPG_OK = 0,

@@ -110,6 +110,62 @@ static double fast_poly(const rpg_model* model, const rpg_poly* p,
   return outer;
 }
 
+/* FAST_CM twin (GPU RPG_ARITH_FAST_CM): the same two steps with the roles  */
+/* swapped.  Per data-exponent pattern the block-dimension part is          */
+/* collapsed in basis order with fma: C = fma(c_k, mB_k, C), mB_k the       */
+/* eval_monomial product over the block variables only (the GPU does this   */
+/* once per configuration when the plan is built); the data part is then a */
+/* nested Horner over the data variables in model order, every step an fma */
+/* (at most three data variables).                                          */
+static double fast_cm_poly(const rpg_model* model, const rpg_poly* p,
+                           const double* x) {
+  const int32_t nv = model->n_vars;
+  int dv[3];
+  int nd = 0;
+  for (int v = 0; v < nv; ++v)
+    if (model->var_kind[v] >= 0 && nd < 3) dv[nd++] = v;
+  int maxd[3] = {0, 0, 0};
+  for (int32_t k = 0; k < p->n_terms; ++k)
+    for (int j = 0; j < nd; ++j) {
+      int e = p->exps[(size_t)k * nv + dv[j]];
+      if (e > maxd[j]) maxd[j] = e;
+    }
+  int s0 = nd > 0 ? maxd[0] + 1 : 1, s1 = nd > 1 ? maxd[1] + 1 : 1,
+      s2 = nd > 2 ? maxd[2] + 1 : 1;
+  double C[(O1_MAXDEG + 1) * (O1_MAXDEG + 1) * (O1_MAXDEG + 1)];
+  for (int i = 0; i < s0 * s1 * s2; ++i) C[i] = 0.0;
+  for (int32_t k = 0; k < p->n_terms; ++k) {
+    const uint8_t* ex = p->exps + (size_t)k * nv;
+    double mB = 1.0;
+    for (int v = 0; v < nv; ++v) {
+      if (model->var_kind[v] >= 0) continue;
+      double pw = 1.0;
+      for (int e = 0; e < ex[v]; ++e) pw *= x[v];
+      mB *= pw;
+    }
+    int a = nd > 0 ? ex[dv[0]] : 0;
+    int b = nd > 1 ? ex[dv[1]] : 0;
+    int c = nd > 2 ? ex[dv[2]] : 0;
+    double* slot = &C[(a * s1 + b) * s2 + c];
+    *slot = fma(p->coef[k], mB, *slot);
+  }
+  double xv0 = nd > 0 ? x[dv[0]] : 0.0;
+  double xv1 = nd > 1 ? x[dv[1]] : 0.0;
+  double xv2 = nd > 2 ? x[dv[2]] : 0.0;
+  double outer = 0.0;
+  for (int a = s0 - 1; a >= 0; --a) {
+    double mid = 0.0;
+    for (int b = s1 - 1; b >= 0; --b) {
+      double inner = C[(a * s1 + b) * s2 + (s2 - 1)];
+      for (int c = s2 - 2; c >= 0; --c)
+        inner = fma(inner, xv2, C[(a * s1 + b) * s2 + c]);
+      mid = (b == s1 - 1) ? inner : fma(mid, xv1, inner);
+    }
+    outer = (a == s0 - 1) ? mid : fma(outer, xv0, mid);
+  }
+  return outer;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Occupancy — perfmodel.hpp:239-266 (direct path).                          */
 
@@ -260,7 +316,10 @@ static int metric_value(const rpg_model* model, int slot, const double* x,
     return 0;
   }
   double p, q;
-  if (fast) {
+  if (fast == RPG_ARITH_FAST_CM) {
+    p = fast_cm_poly(model, &mt->num, x);
+    q = fast_cm_poly(model, &mt->den, x);
+  } else if (fast) {
     p = fast_poly(model, &mt->num, x);
     q = fast_poly(model, &mt->den, x);
   } else {
@@ -413,7 +472,7 @@ int o1_eval_point(const rpg_model* model, const rpg_profile* hw,
                   const rpg_options* opts, const int64_t* data, int32_t d,
                   const rpg_config* c, o1_point* out) {
   (void)d;
-  return eval_point_impl(model, hw, opts, data, c, opts->arith == RPG_ARITH_FAST,
+  return eval_point_impl(model, hw, opts, data, c, opts->arith,
                          out);
 }
 
@@ -478,7 +537,7 @@ static int search_one_impl(const rpg_model* model, const rpg_profile* hw,
                            int64_t n_space, const int64_t* data,
                            rpg_winner* out, int32_t* order, double* ec,
                            int32_t* w_occ, int32_t* idx, o1_point* pts) {
-  int fast = opts->arith == RPG_ARITH_FAST;
+  int fast = opts->arith;  /* RPG_ARITH_*: selects the polynomial order */
   int64_t nf = 0;
   for (int64_t i = 0; i < n_space; ++i) {
     eval_point_impl(model, hw, opts, data, &space[i], fast, &pts[i]);
@@ -567,7 +626,7 @@ static void* search_worker(void* arg) {
 
 static void* evaluate_worker(void* arg) {
   batch_job* j = (batch_job*)arg;
-  int fast = j->opts->arith == RPG_ARITH_FAST;
+  int fast = j->opts->arith;
   for (int64_t t = j->lo; t < j->hi; ++t)
     for (int64_t c = 0; c < j->n_space; ++c) {
       o1_point p;

@@ -22,7 +22,7 @@ RPG_VAR_BX, RPG_VAR_BY, RPG_VAR_BZ = -1, -2, -3
 RPG_CASE_BOTH_SATURATED, RPG_CASE_CWP_BOUND, RPG_CASE_MWP_BOUND, RPG_CASE_UNKNOWN = 0, 1, 2, 3
 CASE_NAMES = {0: "both_saturated", 1: "cwp_bound", 2: "mwp_bound", 3: "-"}
 RPG_REP_REAL, RPG_REP_CEIL = 0, 1
-RPG_ARITH_EXACT, RPG_ARITH_FAST = 0, 1
+RPG_ARITH_EXACT, RPG_ARITH_FAST, RPG_ARITH_FAST_CM = 0, 1, 2
 RPG_KERNEL_SPECIALIZED, RPG_KERNEL_GENERIC = 0, 1
 
 RPG_OK = 0

@@ -23,6 +23,10 @@ struct Module {
 constexpr int kDefaultThreads = 32;
 int jit_threads(bool exact = false);
 int default_min_blocks(int threads);
+// fast_cm plans: threads per CTA (RPG_CM_THREADS, default 256).
+int cm_threads();
+// fast_cm plans: tuples per CTA (RPG_CM_TUPLES, default 16).
+int cm_tuples();
 
 // CUDA source of the specialized kernels for a plan's model.
 std::string generate_source(const rpg::Params& P, const std::vector<double>& coef,

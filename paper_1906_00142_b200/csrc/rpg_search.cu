@@ -68,7 +68,46 @@ __global__ void occ_table_kernel(const __grid_constant__ Params P, int4* __restr
   }
 }
 
-// ---------------------------------------------------------------------------
+// RPG_ARITH_FAST_CM table: per configuration and metric polynomial, the
+// coefficient of each power of D1, C_j = fma(c_k, mB_k, C_j) over the terms
+// in basis order, mB_k = the product over the block variables in model
+// order of x^e built by repeated multiplication (O1 fast_cm_poly).
+__global__ void cm_table_kernel(const __grid_constant__ Params P, double* __restrict__ cm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)P.n_space * (2 * RPG_N_METRICS)) return;
+  const int c = (int)(i / (2 * RPG_N_METRICS));
+  const int s = (int)(i % (2 * RPG_N_METRICS)) >> 1, side = (int)(i & 1);
+  double* row = cm + (size_t)c * P.n_cm;
+  if (s == 0 && side == 0) {  // padding slots
+    const int last = P.cm_deg[RPG_N_METRICS - 1][1];
+    for (int j = P.cm_off[RPG_N_METRICS - 1][1] + (last >= 0 ? last + 1 : 0); j < P.n_cm; ++j)
+      row[j] = 0.0;
+  }
+  const int deg = P.cm_deg[s][side];
+  if (deg < 0) return;
+  const PolyDesc pd = side ? P.metric[s].den : P.metric[s].num;
+  const int4 cf = P.cfg[c];
+  double C[16];
+  for (int j = 0; j <= deg; ++j) C[j] = 0.0;
+  for (int k = pd.term_off; k < pd.term_off + pd.n_terms; ++k) {
+    const uint64_t ex = P.exps[k];
+    double m = 1.0;
+    int jd = 0;
+    for (int v = 0; v < P.n_vars; ++v) {
+      const int kind = P.var_kind[v];
+      const int e = (int)((ex >> (8 * v)) & 0xff);
+      if (kind >= 0) {
+        jd = e;
+        continue;
+      }
+      const double x = kind == RPG_VAR_BX ? (double)cf.x : kind == RPG_VAR_BY ? (double)cf.y
+                                                                               : (double)cf.z;
+      m = __dmul_rn(m, ipow(x, e));
+    }
+    C[jd] = fma(P.coef[k], m, C[jd]);
+  }
+  for (int j = 0; j <= deg; ++j) row[P.cm_off[s][side] + j] = C[j];
+}
 
 int set_err(char* err, size_t errlen, int code, const char* fmt, ...) {
   if (err && errlen) {
@@ -144,6 +183,8 @@ struct rpg_plan {
   double* d_occ_rcp = nullptr;
   int4* d_lean = nullptr;
   double2* d_rep_tab = nullptr;
+  double* d_cm = nullptr;      // RPG_ARITH_FAST_CM per-configuration table
+  int tuples_per_cta = 1;      // FAST_CM: 32 tuples (one per lane) per CTA
   // bare-program plans: first evaluation error (Params::err_flag)
   bool is_program = false;
   long long step_limit = 0;
@@ -215,8 +256,9 @@ int prepare_model(const rpg_model* model, const rpg_profile* hw, const rpg_optio
   if (rc) return rc;
   if (opts->rep_mode != RPG_REP_REAL && opts->rep_mode != RPG_REP_CEIL)
     return set_err(err, errlen, RPG_E_INVALID, "rep_mode must be real or ceil");
-  if (opts->arith != RPG_ARITH_EXACT && opts->arith != RPG_ARITH_FAST)
-    return set_err(err, errlen, RPG_E_INVALID, "arith must be exact or fast");
+  if (opts->arith != RPG_ARITH_EXACT && opts->arith != RPG_ARITH_FAST &&
+      opts->arith != RPG_ARITH_FAST_CM)
+    return set_err(err, errlen, RPG_E_INVALID, "arith must be exact, fast or fast_cm");
   if (opts->kernel != RPG_KERNEL_SPECIALIZED && opts->kernel != RPG_KERNEL_GENERIC)
     return set_err(err, errlen, RPG_E_INVALID, "kernel must be specialized or generic");
   P = Params{};
@@ -329,6 +371,38 @@ int prepare_model(const rpg_model* model, const rpg_profile* hw, const rpg_optio
   P.n_slots = (int32_t)slot_begin.size() - 1;
   P.occ_const = P.metric[RPG_METRIC_REGS].is_const && P.metric[RPG_METRIC_SHARED].is_const;
 
+  if (P.arith == RPG_ARITH_FAST_CM) {
+    // Configuration-major collapse: one data parameter (D1), one slot per
+    // power of D1 up to the polynomial's degree in it (O1's fast_cm_poly).
+    if (opts->kernel != RPG_KERNEL_SPECIALIZED)
+      return set_err(err, errlen, RPG_E_INVALID, "arith fast_cm needs the specialized kernel");
+    if (max_d > 0)
+      return set_err(err, errlen, RPG_E_INVALID,
+                     "arith fast_cm supports models with one data parameter (D1)");
+    if (!P.occ_const)
+      return set_err(err, errlen, RPG_E_INVALID,
+                     "arith fast_cm needs constant register and shared-memory metrics");
+    int off = 0;
+    for (int s = 0; s < RPG_N_METRICS; ++s) {
+      const MetricDesc& md = P.metric[s];
+      for (int side = 0; side < 2; ++side) {
+        P.cm_off[s][side] = off;
+        P.cm_deg[s][side] = -1;
+        if (md.is_const || (side == 1 && md.den_is_one)) continue;
+        const PolyDesc& pd = side ? md.den : md.num;
+        int deg = 0;
+        for (int k = pd.term_off; k < pd.term_off + pd.n_terms; ++k)
+          for (int v = 0; v < nv; ++v)
+            if (P.var_kind[v] == 0) deg = std::max(deg, (int)((exps[k] >> (8 * v)) & 0xff));
+        if (deg > 15)
+          return set_err(err, errlen, RPG_E_MODEL, "arith fast_cm: degree in D1 above 15");
+        P.cm_deg[s][side] = deg;
+        off += deg + 1;
+      }
+    }
+    P.n_cm = std::max(2, (off + 1) & ~1);  // even: rows are read as double2 pairs
+    P.cm_lanes = std::min(rpg_jit::cm_tuples(), rpg_jit::cm_threads());
+  }
   return RPG_OK;
 }
 
@@ -444,6 +518,17 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
   P.rep_tab = plan->d_rep_tab;
   P.err_flag = plan->d_err;
   P.d = 0;
+  if (P.arith == RPG_ARITH_FAST_CM) {
+    if (!P.lean_ok)
+      return fail(set_err(err, errlen, RPG_E_INVALID,
+                          "arith fast_cm: block dimensions or occupancy limits out of range"));
+    PLAN_CUDA(cudaMalloc(&plan->d_cm, sizeof(double) * (size_t)P.n_cm * (size_t)n_space));
+    P.cm = plan->d_cm;
+    const int64_t nthr = n_space * 2 * RPG_N_METRICS;
+    cm_table_kernel<<<(int)((nthr + 255) / 256), 256, 0, plan->stream>>>(P, plan->d_cm);
+    PLAN_CUDA(cudaGetLastError());
+    plan->tuples_per_cta = P.cm_lanes;
+  }
   if (P.occ_const) {
     const int64_t nthr = std::max<int64_t>(n_space, P.lean_ok ? P.hw.B_max + 1 : 0);
     occ_table_kernel<<<(int)((nthr + 255) / 256), 256, 0, plan->stream>>>(
@@ -452,7 +537,8 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     PLAN_CUDA(cudaStreamSynchronize(plan->stream));
   }
 
-  plan->smem = smem_layout(smem_terms(P), P.n_slots, rep_entries(P)).total;
+  plan->smem = P.arith == RPG_ARITH_FAST_CM ? cm_smem_bytes(P, rpg_jit::cm_threads())
+                                           : smem_layout(smem_terms(P), P.n_slots, rep_entries(P)).total;
   int smem_optin = 0;
   PLAN_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   if (plan->smem > (size_t)smem_optin)
@@ -461,7 +547,9 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     std::string jerr;
     // Resident CTAs per SM the specialized kernels are register-budgeted for
     // (launch bounds); RPG_JIT_MIN_BLOCKS overrides it for tuning sweeps.
-    const int threads = rpg_jit::jit_threads(!is_program && P.arith == RPG_ARITH_EXACT);
+    const int threads = P.arith == RPG_ARITH_FAST_CM
+                            ? rpg_jit::cm_threads()
+                            : rpg_jit::jit_threads(!is_program && P.arith == RPG_ARITH_EXACT);
     if (jit(rpg_jit::default_min_blocks(threads), threads, &plan->jit, &jerr) != 0)
       return fail(set_err(err, errlen, RPG_E_CUDA, "%s", jerr.c_str()));
     plan->threads = threads;
@@ -612,6 +700,7 @@ int rpg_plan_destroy(rpg_plan* plan) {
   if (plan->stream) cudaStreamDestroy(plan->stream);
   if (plan->copy_stream) cudaStreamDestroy(plan->copy_stream);
   for (cudaEvent_t e : plan->chunk_done) cudaEventDestroy(e);
+  if (plan->d_cm) cudaFree(plan->d_cm);
   delete plan;  // specialized modules stay cached for the process
   return RPG_OK;
 }
@@ -684,6 +773,14 @@ int check_arity(const rpg_plan* plan, int32_t d, char* err, size_t errlen) {
   return RPG_OK;
 }
 
+// FAST_CM plans serve whole-space searches only.
+int check_not_cm(const rpg_plan* plan, const char* what, char* err, size_t errlen) {
+  if (plan->P.arith == RPG_ARITH_FAST_CM)
+    return set_err(err, errlen, RPG_E_INVALID, "%s: not available with arith fast_cm (searches only)",
+                   what);
+  return RPG_OK;
+}
+
 int launch_search(rpg_plan* plan, const int64_t* d_data, int64_t n, int32_t d,
                   rpg_winner* d_out, cudaStream_t s, char* err, size_t errlen,
                   const int64_t* d_sub_off = nullptr, const int32_t* d_sub_list = nullptr) {
@@ -692,7 +789,8 @@ int launch_search(rpg_plan* plan, const int64_t* d_data, int64_t n, int32_t d,
   P.d = d;
   P.sub_off = d_sub_off;
   P.sub_list = d_sub_list;
-  const int grid = (int)std::min<int64_t>(n, plan->grid_search);
+  const int64_t units = (n + plan->tuples_per_cta - 1) / plan->tuples_per_cta;
+  const int grid = (int)std::min<int64_t>(units, plan->grid_search);
   void* args[] = {&P, &d_data, &n, &d_out};
   CUDA_TRY(cudaLaunchKernel(search_fn(plan), dim3(grid), dim3(plan->threads), args, plan->smem, s));
   return RPG_OK;
@@ -742,7 +840,7 @@ int rpg_search_batch(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int3
   // Large batches run as chunks of whole persistent-grid waves so the D2H of
   // a finished chunk overlaps the kernels of the next ones (no extra tail:
   // every chunk but the last is an exact multiple of the resident grid).
-  const int64_t chunk = 4LL * std::max(1, plan->grid_search);
+  const int64_t chunk = 4LL * std::max(1, plan->grid_search) * plan->tuples_per_cta;
   const int64_t n_chunks = plan->is_program ? 1 : std::max<int64_t>(1, std::min<int64_t>(8, n_tuples / chunk));
   if (n_chunks <= 1) {
     rc = launch_search(plan, plan->d_data, n_tuples, d, (rpg_winner*)plan->d_out, plan->stream,
@@ -754,7 +852,7 @@ int rpg_search_batch(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int3
   }
   // Chunks of `chunk` tuples, the remainder folded into the second-to-last
   // chunk, and a last chunk of one wave so the only exposed copy is small.
-  const int64_t wave = std::max(1, plan->grid_search);
+  const int64_t wave = (int64_t)std::max(1, plan->grid_search) * plan->tuples_per_cta;
   int64_t lo[10], cnt[10];
   int64_t nc = 0;
   for (int64_t at = 0; at < n_tuples;) {
@@ -794,6 +892,7 @@ int rpg_evaluate_device(rpg_plan* plan, const int64_t* d_data, int64_t n_tuples,
   if (!plan) return set_err(err, errlen, RPG_E_INVALID, "null plan");
   int rc = check_arity(plan, d, err, errlen);
   if (rc) return rc;
+  if ((rc = check_not_cm(plan, "rpg_evaluate_device", err, errlen))) return rc;
   CUDA_TRY(cudaSetDevice(plan->device));
   return launch_evaluate(plan, d_data, n_tuples, d, d_ec, d_tag, d_wocc, (cudaStream_t)stream,
                          err, errlen);
@@ -804,6 +903,7 @@ int rpg_evaluate(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int32_t 
   if (!plan) return set_err(err, errlen, RPG_E_INVALID, "null plan");
   int rc = check_arity(plan, d, err, errlen);
   if (rc) return rc;
+  if ((rc = check_not_cm(plan, "rpg_evaluate", err, errlen))) return rc;
   if (n_tuples <= 0) return RPG_OK;
   std::lock_guard<std::mutex> lock(plan->mu);
   CUDA_TRY(cudaSetDevice(plan->device));
@@ -863,6 +963,7 @@ int rpg_search_batch_subsets_device(rpg_plan* plan, const int64_t* d_data, int64
   if (!plan) return set_err(err, errlen, RPG_E_INVALID, "null plan");
   int rc = check_arity(plan, d, err, errlen);
   if (rc) return rc;
+  if ((rc = check_not_cm(plan, "rpg_search_batch_subsets_device", err, errlen))) return rc;
   CUDA_TRY(cudaSetDevice(plan->device));
   return launch_search(plan, d_data, n_tuples, d, d_out, (cudaStream_t)stream, err, errlen,
                        d_offsets, d_list);
@@ -874,6 +975,7 @@ int rpg_search_batch_subsets(rpg_plan* plan, const int64_t* data, int64_t n_tupl
   if (!plan) return set_err(err, errlen, RPG_E_INVALID, "null plan");
   int rc = check_arity(plan, d, err, errlen);
   if (rc) return rc;
+  if ((rc = check_not_cm(plan, "rpg_search_batch_subsets", err, errlen))) return rc;
   if (n_tuples <= 0) return RPG_OK;
   if ((rc = check_subsets(plan, n_tuples, offsets, list, err, errlen))) return rc;
   std::lock_guard<std::mutex> lock(plan->mu);

@@ -32,20 +32,20 @@ class SearchOptions:
     shared_words_per_block: float = 0.0
     rep_mode: str = "real"          # real | ceil
     tie_rel_tol: float = 1e-12
-    arith: str = "exact"            # exact | fast
+    arith: str = "exact"            # exact | fast | fastcm (searches only)
     kernel: str = "specialized"     # specialized (per-model NVRTC kernel) | generic
     device: int = 0
 
     def struct(self) -> A.rpg_options:
         if self.rep_mode not in ("real", "ceil"):
             raise ValueError("rep_mode must be real or ceil")
-        if self.arith not in ("exact", "fast"):
-            raise ValueError("arith must be exact or fast")
+        if self.arith not in ("exact", "fast", "fastcm"):
+            raise ValueError("arith must be exact, fast or fastcm")
         if self.kernel not in ("specialized", "generic"):
             raise ValueError("kernel must be specialized or generic")
         return A.options_struct(
             A.RPG_REP_CEIL if self.rep_mode == "ceil" else A.RPG_REP_REAL,
-            A.RPG_ARITH_FAST if self.arith == "fast" else A.RPG_ARITH_EXACT,
+            {"exact": A.RPG_ARITH_EXACT, "fast": A.RPG_ARITH_FAST, "fastcm": A.RPG_ARITH_FAST_CM}[self.arith],
             self.tie_rel_tol, self.regs_per_thread, self.shared_words_per_block,
             A.RPG_KERNEL_GENERIC if self.kernel == "generic" else A.RPG_KERNEL_SPECIALIZED)
 

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Dump a bench model's specialized kernel source and compile it with nvcc
 (-Xptxas -v) for register / SASS inspection.  Usage:
-  jit_sass.py [gemm|2dconv|atax1] [fast|exact] [min_blocks] [threads]
+  jit_sass.py [gemm|2dconv|atax1] [fast|fastcm|exact] [min_blocks] [threads]
 (defaults: the JIT's — FAST 32 threads x 24 blocks, EXACT 256 x 3)"""
 import ctypes as C
 import os
@@ -15,7 +15,7 @@ from paper_1906_00142_b200 import abi as A, formats as F  # noqa: E402
 
 kern = sys.argv[1] if len(sys.argv) > 1 else "gemm"
 mode = sys.argv[2] if len(sys.argv) > 2 else "fast"
-th = sys.argv[4] if len(sys.argv) > 4 else ("32" if mode == "fast" else "256")
+th = sys.argv[4] if len(sys.argv) > 4 else {"fast": "32", "fastcm": "64"}.get(mode, "256")
 mb = sys.argv[3] if len(sys.argv) > 3 else str(768 // int(th))
 out = "/tmp/rpg_jit_sass"
 os.makedirs(out, exist_ok=True)
@@ -23,7 +23,7 @@ lib = A.load_library()
 spec = F.models_to_metric_spec(F.read_models(os.path.join(ROOT, "data", "polybench", f"{kern}.models.json")))
 pk = A.PackedModel(spec)
 hw = A.profile_struct(F.load_profile(os.path.join(ROOT, "data", "b200.profile")))
-opts = A.options_struct(arith=A.RPG_ARITH_FAST if mode == "fast" else A.RPG_ARITH_EXACT)
+opts = A.options_struct(arith={"fast": A.RPG_ARITH_FAST, "fastcm": A.RPG_ARITH_FAST_CM}.get(mode, A.RPG_ARITH_EXACT))
 buf = C.create_string_buffer(1 << 21)
 err = C.create_string_buffer(4096)
 n = lib.rpg_emit_cuda_source(C.byref(pk.struct), C.byref(hw), C.byref(opts), 0, buf, len(buf), None, err, len(err))
