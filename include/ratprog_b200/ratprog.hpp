@@ -911,7 +911,7 @@ inline ir::RationalProgram generate_rp(const MetricModelSet& models, const perf:
   return rp;
 }
 
-enum class Arith { Exact, Fast };
+enum class Arith { Exact, Fast, FastCM };  // RPG_ARITH_* (rpg.h)
 enum class Kernel { Specialized, Generic };
 
 // pipe::SearchOptions (pipeline.hpp:438-452) + B200 knobs.
@@ -1042,7 +1042,9 @@ inline rpg_profile to_rpg(const perf::DeviceProfile& hw) {
 inline rpg_options to_rpg(const SearchOptions& o) {
   rpg_options r{};
   r.rep_mode = o.rep_mode == perf::RepMode::Ceil ? RPG_REP_CEIL : RPG_REP_REAL;
-  r.arith = o.arith == Arith::Fast ? RPG_ARITH_FAST : RPG_ARITH_EXACT;
+  r.arith = o.arith == Arith::Fast     ? RPG_ARITH_FAST
+            : o.arith == Arith::FastCM ? RPG_ARITH_FAST_CM
+                                       : RPG_ARITH_EXACT;
   r.tie_rel_tol = o.tie_rel_tol;
   r.regs_per_thread = o.regs_per_thread;
   r.shared_words_per_block = o.shared_words_per_block;

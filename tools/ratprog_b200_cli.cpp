@@ -6,7 +6,7 @@
 //       [--format text|csv|json] [-o FILE] [--dump-jsonl FILE]
 //       [--rep-mode real|ceil] [--regs-per-thread R] [--shared-words Z]
 //       [--max-threads T] [--min-threads T] [--dims 1|2|3] [--jobs J]
-//       [--arith exact|fast] [--kernel specialized|generic]
+//       [--arith exact|fast|fastcm] [--kernel specialized|generic]
 //   ratprog-b200 sweep --models M --profile P --from LO --to HI
 //       [--space pow2|dense] [--dims 2|3] [-o FILE] [--arith ...]
 //
@@ -57,7 +57,9 @@ pipe::SearchOptions options(const Args& a) {
   else if (a.rep_mode != "real") throw std::runtime_error("--rep-mode must be 'real' or 'ceil'");
   o.regs_per_thread = a.regs;
   o.shared_words_per_block = a.shared;
-  o.arith = a.arith == "fast" ? pipe::Arith::Fast : pipe::Arith::Exact;
+  o.arith = a.arith == "fast"     ? pipe::Arith::Fast
+            : a.arith == "fastcm" ? pipe::Arith::FastCM
+                                  : pipe::Arith::Exact;
   o.kernel = a.kernel == "generic" ? pipe::Kernel::Generic : pipe::Kernel::Specialized;
   return o;
 }
