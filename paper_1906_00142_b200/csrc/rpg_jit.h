@@ -27,6 +27,8 @@ int default_min_blocks(int threads);
 int cm_threads();
 // fast_cm plans: tuples per CTA (RPG_CM_TUPLES, default 16).
 int cm_tuples();
+// fast_cm plans: two tuples per thread (RPG_CM_PAIR=1; default off).
+int cm_pair();
 
 // CUDA source of the specialized kernels for a plan's model.
 std::string generate_source(const rpg::Params& P, const std::vector<double>& coef,

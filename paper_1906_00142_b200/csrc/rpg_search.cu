@@ -402,6 +402,7 @@ int prepare_model(const rpg_model* model, const rpg_profile* hw, const rpg_optio
     }
     P.n_cm = std::max(2, (off + 1) & ~1);  // even: rows are read as double2 pairs
     P.cm_lanes = std::min(rpg_jit::cm_tuples(), rpg_jit::cm_threads());
+    P.cm_pair = rpg_jit::cm_pair();
   }
   return RPG_OK;
 }
@@ -527,7 +528,7 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     const int64_t nthr = n_space * 2 * RPG_N_METRICS;
     cm_table_kernel<<<(int)((nthr + 255) / 256), 256, 0, plan->stream>>>(P, plan->d_cm);
     PLAN_CUDA(cudaGetLastError());
-    plan->tuples_per_cta = P.cm_lanes;
+    plan->tuples_per_cta = P.cm_lanes * (P.cm_pair ? 2 : 1);
   }
   if (P.occ_const) {
     const int64_t nthr = std::max<int64_t>(n_space, P.lean_ok ? P.hw.B_max + 1 : 0);
@@ -537,7 +538,7 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     PLAN_CUDA(cudaStreamSynchronize(plan->stream));
   }
 
-  plan->smem = P.arith == RPG_ARITH_FAST_CM ? cm_smem_bytes(P, rpg_jit::cm_threads())
+  plan->smem = P.arith == RPG_ARITH_FAST_CM ? cm_smem_bytes(P, rpg_jit::cm_threads() * (P.cm_pair ? 2 : 1))
                                            : smem_layout(smem_terms(P), P.n_slots, rep_entries(P)).total;
   int smem_optin = 0;
   PLAN_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
