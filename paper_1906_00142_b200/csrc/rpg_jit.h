@@ -27,8 +27,10 @@ int default_min_blocks(int threads);
 int cm_threads();
 // fast_cm plans: tuples per CTA (RPG_CM_TUPLES, default 16).
 int cm_tuples();
-// fast_cm plans: two tuples per thread (RPG_CM_PAIR=1; default off).
+// fast_cm plans: two tuples per thread (RPG_CM_PAIR=0 turns it off).
 int cm_pair();
+// fast_cm plans: resident CTAs per SM the kernel is register-budgeted for.
+int cm_min_blocks(int threads, bool pair);
 
 // CUDA source of the specialized kernels for a plan's model.
 std::string generate_source(const rpg::Params& P, const std::vector<double>& coef,

@@ -551,7 +551,9 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     const int threads = P.arith == RPG_ARITH_FAST_CM
                             ? rpg_jit::cm_threads()
                             : rpg_jit::jit_threads(!is_program && P.arith == RPG_ARITH_EXACT);
-    if (jit(rpg_jit::default_min_blocks(threads), threads, &plan->jit, &jerr) != 0)
+    const int min_blocks = P.arith == RPG_ARITH_FAST_CM ? rpg_jit::cm_min_blocks(threads, P.cm_pair)
+                                                      : rpg_jit::default_min_blocks(threads);
+    if (jit(min_blocks, threads, &plan->jit, &jerr) != 0)
       return fail(set_err(err, errlen, RPG_E_CUDA, "%s", jerr.c_str()));
     plan->threads = threads;
   }
@@ -1044,8 +1046,10 @@ extern "C" int64_t rpg_emit_cuda_source(const rpg_model* model, const rpg_profil
   if (compile) {
     std::vector<char> cubin;
     std::string log;
-    const int threads = rpg_jit::jit_threads(opts->arith == RPG_ARITH_EXACT);
-    if (rpg_jit::compile(src, rpg_jit::default_min_blocks(threads), threads, &cubin, &log) != 0)
+    const bool cm = opts->arith == RPG_ARITH_FAST_CM;
+    const int threads = cm ? rpg_jit::cm_threads() : rpg_jit::jit_threads(opts->arith == RPG_ARITH_EXACT);
+    const int mb = cm ? rpg_jit::cm_min_blocks(threads, P.cm_pair) : rpg_jit::default_min_blocks(threads);
+    if (rpg_jit::compile(src, mb, threads, &cubin, &log) != 0)
       return set_err(err, errlen, RPG_E_CUDA, "NVRTC: %s", log.substr(0, 1500).c_str());
     if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
   }
