@@ -168,12 +168,17 @@ class Plan:
             a = a.reshape(-1, 1) if self.d <= 1 else a.reshape(1, -1)
         return a
 
-    def search_batch(self, data) -> np.ndarray:
+    def search_batch(self, data, out: Optional[np.ndarray] = None) -> np.ndarray:
         """Winners (structured array, abi.WINNER_DTYPE) for every data tuple
-        (rows of ``data``); host buffers in and out."""
+        (rows of ``data``); host buffers in and out.  ``out``: an optional
+        preallocated C-contiguous WINNER_DTYPE array of n records to fill
+        (e.g. in pinned memory) — returned."""
         a = self._data(data)
         n, d = a.shape
-        out = np.zeros(n, dtype=A.WINNER_DTYPE)
+        if out is None:
+            out = np.zeros(n, dtype=A.WINNER_DTYPE)
+        elif out.dtype != A.WINNER_DTYPE or out.shape != (n,) or not out.flags.c_contiguous:
+            raise ValueError("search_batch: out must be a C-contiguous WINNER_DTYPE array of n records")
         err = C.create_string_buffer(512)
         if self.lowered is not None:
             self.lowered.check_binding(d)

@@ -115,3 +115,17 @@ def test_c2_bench_workload_full():
     for k in ("2dconv", "gemm", "atax1"):
         spec = _models(k)
         _same(_gpu(spec, hw, space, data), _o1(spec, hw, space, data), data)
+
+
+def test_search_batch_out_buffer():
+    """search_batch(out=...) fills a caller-provided (e.g. pinned) array with
+    the same records it would return, and rejects a mismatched one."""
+    spec, hw, space = _models("gemm"), _b200(), F.integer_configs(1024, dims=2)
+    data = np.arange(64, 5000, 37, dtype=np.int64).reshape(-1, 1)
+    with S.Plan(spec, hw, space, S.SearchOptions(arith="fastcm")) as plan:
+        want = plan.search_batch(data)
+        out = np.empty(len(data), dtype=A.WINNER_DTYPE)
+        got = plan.search_batch(data, out=out)
+        assert got is out and np.array_equal(out.view(np.uint8), want.view(np.uint8))
+        with pytest.raises(ValueError):
+            plan.search_batch(data, out=np.empty(len(data) - 1, dtype=A.WINNER_DTYPE))
