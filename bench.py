@@ -124,6 +124,13 @@ def official_flops(spec) -> int:
     return total
 
 
+def default_arith(workload: str, kernel: str) -> str:
+    """The arithmetic mode a workload is benchmarked in: the configuration-
+    major FAST_CM search for the one-data-parameter C2/C3 models (specialized
+    kernels only), FAST otherwise (C5's two data parameters, the Ec dump)."""
+    return "fastcm" if workload in ("c2", "c3") and kernel == "specialized" else "fast"
+
+
 def count_kernel_launches(fn, prefix="rpg_"):
     """Kernels whose name starts with `prefix` that one call of fn launches,
     counted by the CUDA activity trace (torch.profiler / CUPTI) outside the
@@ -692,7 +699,7 @@ def main():
                     help="test mode: all ranks on cuda:0 (with --dist-backend gloo)")
     args = ap.parse_args()
     if args.arith is None:
-        args.arith = "fastcm" if args.workload in ("c2", "c3") and args.kernel == "specialized" else "fast"
+        args.arith = default_arith(args.workload, args.kernel)
     if args.impl == "reference":
         if args.workload == "c4":
             return c4_reference_arm(args)

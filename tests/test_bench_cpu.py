@@ -75,3 +75,11 @@ def test_c4_data_shapes_and_reference_arm():
     assert r.returncode == 0, r.stderr[-2000:]
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["impl"] == "reference" and d["unit"] == "samples/s" and d["value"] > 0
+
+
+def test_default_arith_per_workload():
+    assert bench.default_arith("c2", "specialized") == "fastcm"
+    assert bench.default_arith("c3", "specialized") == "fastcm"
+    assert bench.default_arith("c5", "specialized") == "fast"
+    assert bench.default_arith("dump", "specialized") == "fast"
+    assert bench.default_arith("c2", "generic") == "fast"
