@@ -23,9 +23,9 @@ struct Module {
 constexpr int kDefaultThreads = 32;
 int jit_threads(bool exact = false);
 int default_min_blocks(int threads);
-// fast_cm plans: threads per CTA (RPG_CM_THREADS, default 256).
+// fast_cm plans: threads per CTA (RPG_CM_THREADS, default 512).
 int cm_threads();
-// fast_cm plans: tuples per CTA (RPG_CM_TUPLES, default 16).
+// fast_cm plans: tuple lanes per CTA (RPG_CM_TUPLES, default 32).
 int cm_tuples();
 // fast_cm plans: two tuples per thread (RPG_CM_PAIR=0 turns it off).
 int cm_pair();
