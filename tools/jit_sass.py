@@ -2,7 +2,7 @@
 """Dump a bench model's specialized kernel source and compile it with nvcc
 (-Xptxas -v) for register / SASS inspection.  Usage:
   jit_sass.py [gemm|2dconv|atax1] [fast|fastcm|exact] [min_blocks] [threads]
-(defaults: the JIT's — FAST 32 threads x 24 blocks, EXACT 256 x 3)"""
+(defaults: the JIT's — FAST 32 threads x 24 blocks, FASTCM 512 x 1, EXACT 256 x 3)"""
 import ctypes as C
 import os
 import shutil
@@ -15,8 +15,8 @@ from paper_1906_00142_b200 import abi as A, formats as F  # noqa: E402
 
 kern = sys.argv[1] if len(sys.argv) > 1 else "gemm"
 mode = sys.argv[2] if len(sys.argv) > 2 else "fast"
-th = sys.argv[4] if len(sys.argv) > 4 else {"fast": "32", "fastcm": "64"}.get(mode, "256")
-mb = sys.argv[3] if len(sys.argv) > 3 else str(768 // int(th))
+th = sys.argv[4] if len(sys.argv) > 4 else {"fast": "32", "fastcm": "512"}.get(mode, "256")
+mb = sys.argv[3] if len(sys.argv) > 3 else str((512 if mode == "fastcm" else 768) // int(th))
 out = "/tmp/rpg_jit_sass"
 os.makedirs(out, exist_ok=True)
 lib = A.load_library()
