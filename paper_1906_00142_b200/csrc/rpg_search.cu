@@ -261,6 +261,8 @@ int prepare_model(const rpg_model* model, const rpg_profile* hw, const rpg_optio
     return set_err(err, errlen, RPG_E_INVALID, "arith must be exact, fast or fast_cm");
   if (opts->kernel != RPG_KERNEL_SPECIALIZED && opts->kernel != RPG_KERNEL_GENERIC)
     return set_err(err, errlen, RPG_E_INVALID, "kernel must be specialized or generic");
+  if (!std::isfinite(opts->tie_rel_tol) || opts->tie_rel_tol < 0.0)
+    return set_err(err, errlen, RPG_E_INVALID, "tie_rel_tol must be finite and non-negative");
   P = Params{};
   P.hw = *hw;
   hoist_hardware(P);
@@ -624,6 +626,8 @@ int prepare_program(const rpg_program* prog, const rpg_profile* hw, const rpg_op
     if (!std::isfinite(prog->literals[i]))
       return set_err(err, errlen, RPG_E_INVALID, "program literal %d is not finite as a double", i);
 
+  if (!std::isfinite(opts->tie_rel_tol) || opts->tie_rel_tol < 0.0)
+    return set_err(err, errlen, RPG_E_INVALID, "tie_rel_tol must be finite and non-negative");
   P = Params{};
   P.hw = *hw;
   hoist_hardware(P);

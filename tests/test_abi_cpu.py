@@ -157,3 +157,17 @@ def test_specialized_kernel_source_compiles_for_sm100a(arith):
     assert "rpg_jit_search" in src and "rpg_jit_evaluate" in src
     assert ("fma(" in src) == (arith == A.RPG_ARITH_FAST)
     assert cubin.value > 10000
+
+
+@pytest.mark.parametrize("tol", [-1e-12, float("nan"), float("inf")])
+def test_plan_create_rejects_bad_tie_tolerance(tol):
+    lib = A.load_library()
+    spec = F.kernel_to_metric_spec(F.load_kernel_spec(os.path.join(ROOT, "data", "stencil2d.kernel.json")))
+    pk = A.PackedModel(spec)
+    hw = A.profile_struct(F.load_profile(os.path.join(ROOT, "data", "sample_device.profile")))
+    space = A.config_array(F.enumerate_configs())
+    err = C.create_string_buffer(256)
+    h = C.c_void_p()
+    rc = lib.rpg_plan_create(C.byref(pk.struct), C.byref(hw), A.ptr(space, A.rpg_config), len(space),
+                             C.byref(A.options_struct(tie_rel_tol=tol)), 0, C.byref(h), err, 256)
+    assert rc == A.RPG_E_INVALID and b"tie_rel_tol" in err.value

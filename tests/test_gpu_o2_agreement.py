@@ -35,7 +35,7 @@ def _agree(spec, hw, space, ns, arith):
             assert g == feas[0], (n, space[g], space[feas[0]])
 
 
-@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("arith", ["exact", "fast", "fastcm"])
 def test_c1_stencil2d_paper_subset(arith):
     spec = F.kernel_to_metric_spec(F.load_kernel_spec(os.path.join(ROOT, "data", "stencil2d.kernel.json")))
     hw = F.load_profile(os.path.join(ROOT, "data", "sample_device.profile"))
@@ -43,7 +43,7 @@ def test_c1_stencil2d_paper_subset(arith):
 
 
 @pytest.mark.parametrize("kernel", ["2dconv", "gemm", "atax1"])
-@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("arith", ["exact", "fast", "fastcm"])
 def test_c2_models_sampled(kernel, arith):
     spec = F.models_to_metric_spec(F.read_models(os.path.join(ROOT, "data", "polybench", f"{kernel}.models.json")))
     hw = F.load_profile(os.path.join(ROOT, "data", "b200.profile"))

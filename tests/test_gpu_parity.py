@@ -143,3 +143,25 @@ def test_large_space_3d(kernel):
         got = plan.search_batch(data)
     want = _oracle(c, "exact", "search")
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("tol", [0.0, 1e-12])
+@pytest.mark.parametrize("arith,kernel", [("exact", "specialized"), ("fast", "specialized"),
+                                          ("exact", "generic"), ("fast", "generic"), ("fastcm", "specialized")])
+def test_infinite_cycle_estimates_and_empty_tie_group(tol, arith, kernel):
+    """Every feasible Ec is +inf (an overflowing metric).  With tol = 0 the
+    tie bound is inf + inf*0 = NaN, the tie group is empty and the ranking's
+    head is the lowest (Ec, lex) config with ties = 0 (O1, and the
+    reference's sort); with tol > 0 the group is every config.  Records
+    bit-identical to O1 either way."""
+    from .zoo import b200_hw, const_spec
+    hw, space = b200_hw(), F.enumerate_configs()
+    data = np.array([[100], [2000]], dtype=np.int64)
+    for comp, unc, coal, syn, tb in [(1e308, 1, 1, 1, 1), (1, 1e308, 1e308, 1, 1), (1, 1, 1, 1, 1e308)]:
+        spec = const_spec(comp, unc, coal, syn, tb)
+        opts = S.SearchOptions(arith=arith, kernel=kernel, tie_rel_tol=tol)
+        want = o1.search_batch(A.PackedModel(spec, drop_zero_terms=False), A.profile_struct(hw), opts.struct(),
+                               A.config_array(space), data, 2)
+        with S.Plan(spec, hw, space, opts) as plan:
+            got = plan.search_batch(data)
+        assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), (got, want)
