@@ -27,10 +27,13 @@ int default_min_blocks(int threads);
 int cm_threads();
 // fast_cm plans: tuple lanes per CTA (RPG_CM_TUPLES, default 32).
 int cm_tuples();
-// fast_cm plans: two tuples per thread (RPG_CM_PAIR=0 turns it off).
-int cm_pair();
+// fast_cm plans: tuples per thread, 1..4 (RPG_CM_J; RPG_CM_PAIR=0 means 1).
+int cm_j();
+// fast_cm plans: the branch-free pass-1 body search_body_cmj (RPG_CM_SCAN=0
+// selects the round-1 bodies search_body_cm / search_body_cm2, J <= 2).
+int cm_scan();
 // fast_cm plans: resident CTAs per SM the kernel is register-budgeted for.
-int cm_min_blocks(int threads, bool pair);
+int cm_min_blocks(int threads, int j);
 
 // CUDA source of the specialized kernels for a plan's model.
 std::string generate_source(const rpg::Params& P, const std::vector<double>& coef,

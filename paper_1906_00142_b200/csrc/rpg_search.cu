@@ -404,7 +404,9 @@ int prepare_model(const rpg_model* model, const rpg_profile* hw, const rpg_optio
     }
     P.n_cm = std::max(2, (off + 1) & ~1);  // even: rows are read as double2 pairs
     P.cm_lanes = std::min(rpg_jit::cm_tuples(), rpg_jit::cm_threads());
-    P.cm_pair = rpg_jit::cm_pair();
+    P.cm_j = rpg_jit::cm_j();
+    P.cm_scan = rpg_jit::cm_scan();
+    if (!P.cm_scan && P.cm_j > 2) P.cm_j = 2;
   }
   return RPG_OK;
 }
@@ -530,7 +532,7 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     const int64_t nthr = n_space * 2 * RPG_N_METRICS;
     cm_table_kernel<<<(int)((nthr + 255) / 256), 256, 0, plan->stream>>>(P, plan->d_cm);
     PLAN_CUDA(cudaGetLastError());
-    plan->tuples_per_cta = P.cm_lanes * (P.cm_pair ? 2 : 1);
+    plan->tuples_per_cta = P.cm_lanes * P.cm_j;
   }
   if (P.occ_const) {
     const int64_t nthr = std::max<int64_t>(n_space, P.lean_ok ? P.hw.B_max + 1 : 0);
@@ -540,8 +542,9 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     PLAN_CUDA(cudaStreamSynchronize(plan->stream));
   }
 
-  plan->smem = P.arith == RPG_ARITH_FAST_CM ? cm_smem_bytes(P, rpg_jit::cm_threads() * (P.cm_pair ? 2 : 1))
-                                           : smem_layout(smem_terms(P), P.n_slots, rep_entries(P)).total;
+  plan->smem = P.arith == RPG_ARITH_FAST_CM
+                   ? std::max(cm_smem_bytes(P, rpg_jit::cm_threads() * P.cm_j), cm_eval_smem_bytes(P))
+                   : smem_layout(smem_terms(P), P.n_slots, rep_entries(P)).total;
   int smem_optin = 0;
   PLAN_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   if (plan->smem > (size_t)smem_optin)
@@ -553,7 +556,7 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     const int threads = P.arith == RPG_ARITH_FAST_CM
                             ? rpg_jit::cm_threads()
                             : rpg_jit::jit_threads(!is_program && P.arith == RPG_ARITH_EXACT);
-    const int min_blocks = P.arith == RPG_ARITH_FAST_CM ? rpg_jit::cm_min_blocks(threads, P.cm_pair)
+    const int min_blocks = P.arith == RPG_ARITH_FAST_CM ? rpg_jit::cm_min_blocks(threads, P.cm_j)
                                                       : rpg_jit::default_min_blocks(threads);
     if (jit(min_blocks, threads, &plan->jit, &jerr) != 0)
       return fail(set_err(err, errlen, RPG_E_CUDA, "%s", jerr.c_str()));
@@ -780,10 +783,10 @@ int check_arity(const rpg_plan* plan, int32_t d, char* err, size_t errlen) {
   return RPG_OK;
 }
 
-// FAST_CM plans serve whole-space searches only.
+// FAST_CM plans serve whole-space searches and evaluations (no subsets).
 int check_not_cm(const rpg_plan* plan, const char* what, char* err, size_t errlen) {
   if (plan->P.arith == RPG_ARITH_FAST_CM)
-    return set_err(err, errlen, RPG_E_INVALID, "%s: not available with arith fast_cm (searches only)",
+    return set_err(err, errlen, RPG_E_INVALID, "%s: not available with arith fast_cm (whole-space searches and evaluations only)",
                    what);
   return RPG_OK;
 }
@@ -808,7 +811,11 @@ int launch_evaluate(rpg_plan* plan, const int64_t* d_data, int64_t n, int32_t d,
   if (n <= 0) return RPG_OK;
   Params P = plan->P;
   P.d = d;
-  const int grid = (int)std::min<int64_t>(n, plan->grid_eval);
+  int64_t units = n;
+  if (P.arith == RPG_ARITH_FAST_CM)  // evaluate_body_cm tiles: 32 configs x (warps x 4) tuples
+    units = (P.n_space + 31) / 32 *
+            ((n + (plan->threads / 32) * kCmEvalTuplesPerWarp - 1) / ((plan->threads / 32) * kCmEvalTuplesPerWarp));
+  const int grid = (int)std::min<int64_t>(units, plan->grid_eval);
   void* args[] = {&P, &d_data, &n, &ec, &tag, &wocc};
   CUDA_TRY(cudaLaunchKernel(evaluate_fn(plan), dim3(grid), dim3(plan->threads), args, plan->smem, s));
   return RPG_OK;
@@ -899,7 +906,6 @@ int rpg_evaluate_device(rpg_plan* plan, const int64_t* d_data, int64_t n_tuples,
   if (!plan) return set_err(err, errlen, RPG_E_INVALID, "null plan");
   int rc = check_arity(plan, d, err, errlen);
   if (rc) return rc;
-  if ((rc = check_not_cm(plan, "rpg_evaluate_device", err, errlen))) return rc;
   CUDA_TRY(cudaSetDevice(plan->device));
   return launch_evaluate(plan, d_data, n_tuples, d, d_ec, d_tag, d_wocc, (cudaStream_t)stream,
                          err, errlen);
@@ -910,7 +916,6 @@ int rpg_evaluate(rpg_plan* plan, const int64_t* data, int64_t n_tuples, int32_t 
   if (!plan) return set_err(err, errlen, RPG_E_INVALID, "null plan");
   int rc = check_arity(plan, d, err, errlen);
   if (rc) return rc;
-  if ((rc = check_not_cm(plan, "rpg_evaluate", err, errlen))) return rc;
   if (n_tuples <= 0) return RPG_OK;
   std::lock_guard<std::mutex> lock(plan->mu);
   CUDA_TRY(cudaSetDevice(plan->device));
@@ -1052,7 +1057,7 @@ extern "C" int64_t rpg_emit_cuda_source(const rpg_model* model, const rpg_profil
     std::string log;
     const bool cm = opts->arith == RPG_ARITH_FAST_CM;
     const int threads = cm ? rpg_jit::cm_threads() : rpg_jit::jit_threads(opts->arith == RPG_ARITH_EXACT);
-    const int mb = cm ? rpg_jit::cm_min_blocks(threads, P.cm_pair) : rpg_jit::default_min_blocks(threads);
+    const int mb = cm ? rpg_jit::cm_min_blocks(threads, P.cm_j) : rpg_jit::default_min_blocks(threads);
     if (rpg_jit::compile(src, mb, threads, &cubin, &log) != 0)
       return set_err(err, errlen, RPG_E_CUDA, "NVRTC: %s", log.substr(0, 1500).c_str());
     if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();

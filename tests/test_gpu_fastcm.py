@@ -101,7 +101,62 @@ def test_unsupported_plans_fail_loudly():
         S.Plan(c5, hw, F.integer_configs(1024, dims=3), S.SearchOptions(arith="fastcm"))
     with S.Plan(_models("gemm"), hw, space, S.SearchOptions(arith="fastcm")) as plan:
         with pytest.raises(ValueError, match="fast_cm"):
-            plan.evaluate(np.array([[1024]], dtype=np.int64))
+            plan.search_batch_subsets(np.array([[1024]], dtype=np.int64), [0, 1], [0])
+
+
+def _o1_eval(spec, hw, space, data, rep="real", regs=0.0, shared=0.0):
+    opts = S.SearchOptions(arith="fastcm", rep_mode=rep, regs_per_thread=regs,
+                           shared_words_per_block=shared)
+    return o1.evaluate_batch(A.PackedModel(spec, drop_zero_terms=False), A.profile_struct(hw), opts.struct(),
+                             A.config_array(space), data, _threads())
+
+
+def _eval_same(spec, hw, space, data, rep="real", regs=0.0):
+    opts = S.SearchOptions(arith="fastcm", rep_mode=rep, regs_per_thread=regs)
+    with S.Plan(spec, hw, space, opts) as plan:
+        ec, tag, wocc = plan.evaluate(data)
+        win = plan.search_batch(data)
+    oec, otag, owocc = _o1_eval(spec, hw, space, data, rep, regs)
+    assert np.array_equal(ec.view(np.int64), oec.view(np.int64)), np.argwhere(ec.view(np.int64) != oec.view(np.int64))[:5]
+    assert np.array_equal(tag, otag) and np.array_equal(wocc, owocc)
+    # The full ranking from the table heads with the search's winner.
+    for t in range(min(len(data), 6)):
+        res = S.ranking_from_table(A.config_array(space), ec[t], tag[t], wocc[t], hw.W_max, 1e-12)
+        if win["cfg_idx"][t] >= 0:
+            assert res.ranking[0].config == tuple(int(v) for v in A.config_array(space)[win["cfg_idx"][t]])
+            assert res.ties == win["ties"][t]
+
+
+@pytest.mark.parametrize("kernel", ["2dconv", "gemm", "atax1"])
+def test_evaluate_table_c2_models(kernel):
+    """rpg_evaluate in the headline arithmetic (the Ec dump): every point
+    bit-identical to O1's FAST_CM twin; the ranking of the table heads with
+    the search's winner."""
+    spec, hw, space = _models(kernel), _b200(), F.integer_configs(1024, dims=2)
+    data = np.arange(64, 65537, 2731, dtype=np.int64).reshape(-1, 1)  # 24 N (not a multiple of the tile)
+    _eval_same(spec, hw, space, data)
+
+
+@pytest.mark.parametrize("seed", [s for s in range(24) if s % 3 and s % 4])
+def test_evaluate_random_models(seed):
+    spec, hw, space, data, rep = _case(seed)
+    _eval_same(spec, hw, space, data, rep, 24.0)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_evaluate_division_edges(seed):
+    spec, hw, space, data, rep = _edge_case(seed)
+    _eval_same(spec, hw, space, data, rep, 24.0)
+
+
+def test_search_optimal_single_tuple_fastcm():
+    """search_optimal (one tuple, full ranking) in the headline arithmetic."""
+    spec, hw, space = _models("gemm"), _b200(), F.integer_configs(1024, dims=2)
+    res = S.search_optimal(spec, [4096], hw, space, S.SearchOptions(arith="fastcm"))
+    with S.Plan(spec, hw, space, S.SearchOptions(arith="fastcm")) as plan:
+        w = plan.search_batch(np.array([[4096]], dtype=np.int64))[0]
+    assert res.ranking[0].config == tuple(int(v) for v in A.config_array(space)[w["cfg_idx"]])
+    assert len(res.ranking) == w["n_feasible"] and res.evaluated == len(space)
 
 
 def test_c2_bench_workload_full():

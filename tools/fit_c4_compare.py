@@ -1,0 +1,139 @@
+#!/usr/bin/env python
+"""C4 fit parity report: the exact bench arrays
+(10^6 samples of the synthetic GEMM kernel's 5 metrics, variables (D1, bx,
+by), bounds num (2,2,2) / den (1,1,1), seed 1906 — tools/bench_fit.py and
+bench.py --workload c4 draw the same arrays) fitted by the GPU
+(rpg_fit_rational) and by oracle O3, metric by metric: outcome (fitted or
+the failure message), safeguard decision, numerical rank, smallest and
+largest singular value, and the relative difference of the two fitted
+functions on a holdout.
+
+  python tools/fit_c4_compare.py [--noise 0.01] [--samples N] [--o3 live|FIXTURE.json|none]
+  python tools/fit_c4_compare.py --write-fixture tests/golden/c4_o3_noisy.json --noise 0.01
+
+--write-fixture runs O3 only (CPU) and stores its outcomes; the GPU test
+tests/test_gpu_fit_c4.py compares the GPU against those fixtures."""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1906_00142_b200 import formats as F  # noqa: E402
+
+
+def c4_arrays(m=1_000_000, noise=0.0, seed=1906):
+    """The C4 sample arrays (identical to tools/bench_fit.py's draws)."""
+    from oracle import o3_fit as O3
+    rng = np.random.default_rng(seed)
+    D = rng.integers(64, 65537, m).astype(float)
+    cfg = np.array(F.integer_configs(), dtype=float)[rng.integers(0, 7262, m)][:, :2]
+    X = np.ascontiguousarray(np.column_stack([D, cfg]))
+    spec = F.load_kernel_spec(os.path.join(ROOT, "data", "polybench", "gemm.kernel.json"))
+    ys = {}
+    for name in F.REQUIRED_METRICS:
+        y = O3.eval_ratfunc(spec.ground_truth[name], X)
+        if noise > 0:
+            y = y * (1 + rng.uniform(-noise, noise, m))
+        ys[name] = np.ascontiguousarray(y)
+    return X, ys, spec.variables
+
+
+def holdout_points(n=20000, seed=77):
+    rng = np.random.default_rng(seed)
+    D = rng.integers(64, 65537, n).astype(float)
+    cfg = np.array(F.integer_configs(), dtype=float)[rng.integers(0, 7262, n)][:, :2]
+    return np.column_stack([D, cfg])
+
+
+def outcome(fit_fn, X, y, variables, exc):
+    t0 = time.perf_counter()
+    try:
+        f, rep = fit_fn(X, y, variables, [2, 2, 2], [1, 1, 1])
+    except exc as e:
+        return {"status": "failed", "message": str(e), "seconds": time.perf_counter() - t0}
+    sig = [float(s) for s in rep.singular_values]
+    return {"status": "fitted", "safeguard": bool(rep.safeguard), "rank": int(rep.numerical_rank),
+            "truncated": bool(rep.truncated), "sigma_min": sig[-1], "sigma_1": sig[0], "sigma": sig,
+            "num": [float(c) for c in f.num.coeffs], "den": [float(c) for c in f.den.coeffs],
+            "seconds": time.perf_counter() - t0}
+
+
+def ratfunc_values(o, X):
+    from oracle import o3_fit as O3
+    nb, db = F.monomial_basis([2, 2, 2]), F.monomial_basis([1, 1, 1])
+    p = O3.eval_monomials(nb, X) @ np.array(o["num"])
+    q = O3.eval_monomials(db, X) @ np.array(o["den"])
+    return p / q
+
+
+def compare(g, c, H):
+    """Differences between a GPU and an O3 outcome (JSON-able)."""
+    d = {"same_status": g["status"] == c["status"]}
+    if g["status"] == c["status"] == "fitted":
+        d["same_safeguard"] = g["safeguard"] == c["safeguard"]
+        d["same_rank"] = g["rank"] == c["rank"]
+        s1 = c["sigma_1"]
+        d["sigma_max_abs_diff_over_sigma1"] = float(np.max(np.abs(np.array(g["sigma"]) - np.array(c["sigma"]))) / s1)
+        vg, vc = ratfunc_values(g, H), ratfunc_values(c, H)
+        d["holdout_max_rel_diff"] = float(np.max(np.abs(vg - vc) / np.maximum(np.abs(vc), 1e-300)))
+        cg = np.array(g["num"] + g["den"])
+        cc = np.array(c["num"] + c["den"])
+        d["coef_max_abs_diff"] = float(np.max(np.abs(cg - cc)))
+    elif g["status"] == c["status"] == "failed":
+        d["same_message"] = g["message"] == c["message"]
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--samples", type=int, default=1_000_000)
+    ap.add_argument("--noise", type=float, default=0.0)
+    ap.add_argument("--o3", default="fixture", help="live | fixture | none | path.json")
+    ap.add_argument("--write-fixture", default=None)
+    args = ap.parse_args()
+    X, ys, variables = c4_arrays(args.samples, args.noise)
+    from oracle import o3_fit as O3
+    if args.write_fixture:
+        out = {"samples": args.samples, "noise": args.noise, "seed": 1906,
+               "generator": "tools/fit_c4_compare.py --write-fixture", "metrics": {}}
+        for name in sorted(ys):
+            out["metrics"][name] = outcome(O3.fit_rational, X, ys[name], variables, O3.DegenerateFit)
+            print(name, out["metrics"][name]["status"], flush=True)
+        with open(args.write_fixture, "w") as f:
+            json.dump(out, f, indent=1)
+        return
+    from paper_1906_00142_b200 import fit as G
+    o3 = None
+    if args.o3 == "fixture":
+        tag = "clean" if args.noise == 0 else "noisy"
+        path = os.path.join(ROOT, "tests", "golden", f"c4_o3_{tag}.json")
+        if args.samples == 1_000_000 and os.path.exists(path):
+            o3 = json.load(open(path))["metrics"]
+    elif args.o3 not in ("none", "live"):
+        o3 = json.load(open(args.o3))["metrics"]
+    H = holdout_points()
+    rows = {}
+    for name in sorted(ys):
+        g = outcome(G.fit_rational, X, ys[name], variables, (G.DegenerateFit, G.SvdFailure))
+        if args.o3 == "live":
+            c = outcome(O3.fit_rational, X, ys[name], variables, O3.DegenerateFit)
+        else:
+            c = o3[name] if o3 else None
+        row = {"gpu": {k: v for k, v in g.items() if k not in ("sigma",)}}
+        if c is not None:
+            row["o3"] = {k: v for k, v in c.items() if k not in ("sigma",)}
+            row["diff"] = compare(g, c, H)
+        rows[name] = row
+        print(name, json.dumps(row.get("diff", {})), "gpu", g["status"], g.get("safeguard"), g.get("message", ""),
+              flush=True)
+    print(json.dumps({"c4_fit_compare": rows, "noise": args.noise, "samples": args.samples}))
+
+
+if __name__ == "__main__":
+    main()
