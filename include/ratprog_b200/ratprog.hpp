@@ -41,6 +41,8 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <string_view>
+#include <cctype>
 #include <vector>
 
 #include "rpg.h"
@@ -251,20 +253,19 @@ inline const char* case_name(CaseTag t) {
   return "?";
 }
 
-// perf::MwpCwpBreakdown (perfmodel.hpp:284-296).  The GPU direct-model kernel
-// exports b_active, N, the case and the total; the intermediate terms are
-// not exported and stay NaN.
+// perf::MwpCwpBreakdown (perfmodel.hpp:284-296): every field is filled by
+// the GPU direct model (rpg_mwpcwp_breakdown_batch).
 struct MwpCwpBreakdown {
   long long b_active = 0;
   long long n_active_warps = 0;
-  double mem_cycles = NAN;
-  double comp_cycles = NAN;
-  double mwp = NAN;
-  double cwp = NAN;
-  double rep = NAN;
+  double mem_cycles = 0;
+  double comp_cycles = 0;
+  double mwp = 0;
+  double cwp = 0;
+  double rep = 0;
   CaseTag case_tag = CaseTag::CwpBound;
-  double cycles_pre_synch = NAN;
-  double synch_cost = NAN;
+  double cycles_pre_synch = 0;
+  double synch_cost = 0;
   double total_cycles = 0;
 };
 
@@ -326,29 +327,44 @@ inline double occupancy(const DeviceProfile& hw, double R, double Z, long long T
          static_cast<double>(hw.W_max);
 }
 
-// perf::mwpcwp_cycles (perfmodel.hpp:298-395) on the GPU.  Same exceptions:
-// ModelError for negative or inconsistent metrics, ZeroOccupancy when no
-// block fits.
+// perf::mwpcwp_cycles (perfmodel.hpp:298-395) on the GPU, the full
+// breakdown.  Same exceptions in the same order: ModelError for inconsistent
+// or negative metrics, ZeroOccupancy when no block or no warp is resident.
 inline MwpCwpBreakdown mwpcwp_cycles(const DeviceProfile& hw, const KernelMetrics& m,
                                      const LaunchConfig& config, RepMode mode = RepMode::Real) {
-  const double sum = m.uncoal_mem_insts_per_thread + m.coal_mem_insts_per_thread;
-  if (std::fabs(sum - m.mem_insts_per_thread) > 1e-9 * std::max(1.0, m.mem_insts_per_thread))
-    throw ModelError("metrics inconsistent: uncoal + coal must equal mem_insts");
-  int32_t b = 0, w = 0, st = 0;
-  uint8_t tag = 0;
-  double tot = 0;
-  detail::direct_row(hw, m, config, mode, &tot, &b, &w, &tag, &st);
-  if (st == 2 || st == 3 || m.mem_insts_per_thread < 0) throw ModelError("metrics must be non-negative");
-  if (st == 1)
-    throw ZeroOccupancy(b == 0 ? "configuration cannot launch (no resident block)"
-                               : "configuration yields no resident warp");
+  const double km[8] = {m.regs_per_thread, m.shared_words_per_block, m.comp_insts_per_thread,
+                        m.mem_insts_per_thread, m.uncoal_mem_insts_per_thread,
+                        m.coal_mem_insts_per_thread, m.synch_insts_per_block, m.total_blocks};
+  const rpg_profile p = detail::profile_to_rpg(hw);
+  const rpg_config cfg{config.bx, config.by, config.bz};
+  rpg_breakdown o{};
+  char err[512] = {0};
+  const int rc = rpg_mwpcwp_breakdown_batch(
+      &p, km, &cfg, 1, mode == RepMode::Ceil ? RPG_REP_CEIL : RPG_REP_REAL, 0, &o, err, sizeof err);
+  if (rc == RPG_E_PROFILE) throw ProfileError(err);
+  if (rc == RPG_E_INVALID) throw std::invalid_argument(err);
+  if (rc != RPG_OK) throw std::runtime_error(std::string("librpgpu: ") + err);
+  switch (o.status) {
+    case 3: throw ModelError("metrics inconsistent: uncoal + coal must equal mem_insts");
+    case 2: throw ModelError("metrics must be non-negative");
+    case 1: throw ZeroOccupancy("configuration cannot launch (no resident block)");
+    case 4: throw ZeroOccupancy("configuration yields no resident warp");
+    default: break;
+  }
   MwpCwpBreakdown r;
-  r.b_active = b;
-  r.n_active_warps = w;
-  r.case_tag = tag == RPG_CASE_BOTH_SATURATED ? CaseTag::BothSaturated
-               : tag == RPG_CASE_MWP_BOUND   ? CaseTag::MwpBound
-                                             : CaseTag::CwpBound;
-  r.total_cycles = tot;
+  r.b_active = o.b_active;
+  r.n_active_warps = o.n_active_warps;
+  r.mem_cycles = o.mem_cycles;
+  r.comp_cycles = o.comp_cycles;
+  r.mwp = o.mwp;
+  r.cwp = o.cwp;
+  r.rep = o.rep;
+  r.case_tag = o.case_tag == RPG_CASE_BOTH_SATURATED ? CaseTag::BothSaturated
+               : o.case_tag == RPG_CASE_MWP_BOUND   ? CaseTag::MwpBound
+                                                    : CaseTag::CwpBound;
+  r.cycles_pre_synch = o.cycles_pre_synch;
+  r.synch_cost = o.synch_cost;
+  r.total_cycles = o.total_cycles;
   return r;
 }
 
@@ -887,17 +903,382 @@ inline perf::MetricSpec to_metric_spec(const MetricModelSet& m) {
 
 }  // namespace pipe
 
-// The reference's rational program (ir.hpp:19-112) is, on this path, the
-// emitted MWP-CWP program of a metric spec with a profile baked in
-// (pipeline.hpp:233-255).  The B200 build evaluates that program's
-// semantics directly, so the program object carries its spec.
+// ---------------------------------------------------------------------------
+// Rational literals of bare programs.  The reference's Rational is Boost's
+// cpp_rational (rational.hpp:17-19); on the B200 path a literal only ever
+// enters the evaluator as the nearest double (the reference's C lowering
+// prints to_double of each literal, pipeline.hpp:276-433), so the shim keeps
+// the exact value as sign + decimal digit strings (any length) and converts
+// with correct rounding.  No arithmetic is offered on it.
+struct DivisionByZero : std::runtime_error {
+  DivisionByZero() : std::runtime_error("division by zero") {}
+  explicit DivisionByZero(const std::string& what) : std::runtime_error(what) {}
+};
+
+struct Rational {
+  bool negative = false;
+  std::string num = "0", den = "1";  // decimal digits, no leading zeros
+  Rational() = default;
+  Rational(long long v) : negative(v < 0), num(std::to_string(v < 0 ? -(unsigned long long)v : (unsigned long long)v)) {}
+  Rational(long long n, long long d) {
+    if (d == 0) throw DivisionByZero("make_rational: zero denominator");
+    negative = (n < 0) != (d < 0) && n != 0;
+    unsigned long long un = n < 0 ? -(unsigned long long)n : (unsigned long long)n;
+    unsigned long long ud = d < 0 ? -(unsigned long long)d : (unsigned long long)d;
+    const unsigned long long g = std::gcd(un, ud);
+    num = std::to_string(un / g);
+    den = std::to_string(ud / g);
+  }
+  bool operator==(const Rational& o) const {
+    return negative == o.negative && num == o.num && den == o.den;
+  }
+};
+
+namespace detail {
+// Little-endian base-2^32 magnitude, just enough for a correctly rounded
+// num/den -> double: decimal parse, shifts, compare, subtract.
+struct Mag {
+  std::vector<uint32_t> w;
+  static Mag from_decimal(const std::string& s) {
+    Mag m;
+    for (char c : s) {
+      uint64_t carry = (uint64_t)(c - '0');
+      for (uint32_t& x : m.w) {
+        const uint64_t t = (uint64_t)x * 10u + carry;
+        x = (uint32_t)t;
+        carry = t >> 32;
+      }
+      if (carry) m.w.push_back((uint32_t)carry);
+    }
+    return m;
+  }
+  void trim() {
+    while (!w.empty() && w.back() == 0) w.pop_back();
+  }
+  int bits() const {
+    if (w.empty()) return 0;
+    int b = 32 * (int)(w.size() - 1);
+    for (uint32_t t = w.back(); t; t >>= 1) ++b;
+    return b;
+  }
+  void shl(int k) {
+    if (w.empty() || k <= 0) return;
+    const int words = k / 32, r = k % 32;
+    std::vector<uint32_t> o(w.size() + words + 1, 0);
+    for (size_t i = 0; i < w.size(); ++i) {
+      o[i + words] |= w[i] << r;
+      if (r) o[i + words + 1] |= (uint32_t)(w[i] >> (32 - r));
+    }
+    w.swap(o);
+    trim();
+  }
+  void shr1() {
+    for (size_t i = 0; i < w.size(); ++i)
+      w[i] = (w[i] >> 1) | (i + 1 < w.size() ? w[i + 1] << 31 : 0u);
+    trim();
+  }
+  int cmp(const Mag& o) const {
+    if (w.size() != o.w.size()) return w.size() < o.w.size() ? -1 : 1;
+    for (size_t i = w.size(); i-- > 0;)
+      if (w[i] != o.w[i]) return w[i] < o.w[i] ? -1 : 1;
+    return 0;
+  }
+  void sub(const Mag& o) {  // *this >= o
+    int64_t borrow = 0;
+    for (size_t i = 0; i < w.size(); ++i) {
+      int64_t t = (int64_t)w[i] - borrow - (i < o.w.size() ? (int64_t)o.w[i] : 0);
+      borrow = t < 0;
+      w[i] = (uint32_t)(t + (borrow ? (int64_t)1 << 32 : 0));
+    }
+    trim();
+  }
+};
+}  // namespace detail
+
+// Correctly rounded (nearest, ties to even) value of the literal; values in
+// the subnormal range round twice (never produced by the emitted programs).
+inline double to_double(const Rational& r) {
+  detail::Mag n = detail::Mag::from_decimal(r.num), d = detail::Mag::from_decimal(r.den);
+  if (n.w.empty()) return 0.0;
+  // Q = floor(n 2^s / d) with 2^55 <= Q < 2^57; the remainder is the sticky bit.
+  const int s = 56 - (n.bits() - d.bits());
+  if (s > 0) n.shl(s);
+  else d.shl(-s);
+  detail::Mag dd = d;
+  dd.shl(57);
+  uint64_t q = 0;
+  for (int i = 57; i >= 0; --i) {
+    if (n.cmp(dd) >= 0) {
+      n.sub(dd);
+      q |= 1ull << i;
+    }
+    dd.shr1();
+  }
+  const bool sticky = !n.w.empty();
+  int nb = 0;
+  for (uint64_t t = q; t; t >>= 1) ++nb;
+  const int drop = nb - 53;
+  uint64_t mant = q >> drop;
+  const uint64_t rem = q & ((1ull << drop) - 1), half = 1ull << (drop - 1);
+  if (rem > half || (rem == half && (sticky || (mant & 1)))) ++mant;
+  const double v = std::ldexp((double)mant, drop - s);
+  return r.negative ? -v : v;
+}
+
+// parse_rational (rational.hpp:109-148): "n", "n/d" or "i.f", optional '-'.
+inline Rational parse_rational(std::string_view text) {
+  const std::string t(text);
+  auto fail = [&](const char* why) -> Rational {
+    throw std::invalid_argument("bad rational literal '" + t + "': " + why);
+  };
+  if (t.empty()) return fail("empty");
+  size_t i = t[0] == '-' ? 1 : 0;
+  auto digits = [&](std::string* out) {
+    const size_t b = i;
+    while (i < t.size() && std::isdigit((unsigned char)t[i])) ++i;
+    if (i == b) fail("expected digits");
+    *out = t.substr(b, i - b);
+  };
+  auto strip = [](std::string v) {
+    const size_t nz = v.find_first_not_of('0');
+    return nz == std::string::npos ? std::string("0") : v.substr(nz);
+  };
+  Rational r;
+  std::string ip, fp;
+  digits(&ip);
+  if (i < t.size() && t[i] == '/') {
+    ++i;
+    std::string dp;
+    digits(&dp);
+    if (i != t.size()) fail("trailing characters");
+    if (strip(dp) == "0") fail("zero denominator");
+    r.num = strip(ip);
+    r.den = strip(dp);
+  } else if (i < t.size() && t[i] == '.') {
+    ++i;
+    digits(&fp);
+    if (i != t.size()) fail("trailing characters");
+    r.num = strip(ip + fp);
+    r.den = "1" + std::string(fp.size(), '0');
+  } else {
+    if (i != t.size()) fail("trailing characters");
+    r.num = strip(ip);
+  }
+  r.negative = t[0] == '-' && r.num != "0";
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// ir: three-address-code rational programs (ir.hpp:19-112) and their text
+// form (ir_text.hpp).  A program produced by pipe::generate_rp additionally
+// carries the metric spec it was generated from (`spec`): the GPU evaluates
+// that program's semantics with the template kernels.  A bare program
+// (spec == nullptr, e.g. parsed from a `.rp` file) is lowered for
+// rpg_program_plan_create and evaluated by its own generated kernel.
 namespace ir {
+
+enum class Opcode {
+  Assign, Neg, Add, Sub, Mul, EuclidQuot, EuclidRem, FloorDiv, CeilDiv, CmpEq, CmpLt,
+  BranchIf, Jump, HaltReturn
+};
+
+inline const char* opcode_name(Opcode op) {
+  static const char* const names[] = {"assign",    "neg",       "add",       "sub",
+                                      "mul",       "euclid_quot", "euclid_rem", "floor_div",
+                                      "ceil_div",  "cmp_eq",    "cmp_lt",    "branch_if",
+                                      "jump",      "halt_return"};
+  const int i = static_cast<int>(op);
+  return i >= 0 && i < 14 ? names[i] : "?";
+}
+
+struct Operand {
+  enum class Kind { Variable, Literal };
+  Kind kind = Kind::Literal;
+  std::string var;
+  Rational lit;
+  static Operand variable(std::string name) {
+    Operand o;
+    o.kind = Kind::Variable;
+    o.var = std::move(name);
+    return o;
+  }
+  static Operand literal(Rational value) {
+    Operand o;
+    o.lit = std::move(value);
+    return o;
+  }
+  bool is_var() const { return kind == Kind::Variable; }
+  bool operator==(const Operand& o) const {
+    return kind == o.kind && var == o.var && lit == o.lit;
+  }
+};
+
+inline Operand var(std::string name) { return Operand::variable(std::move(name)); }
+inline Operand lit(Rational value) { return Operand::literal(std::move(value)); }
+inline Operand lit(long long value) { return Operand::literal(Rational(value)); }
+
+struct TacInstruction {
+  Opcode op = Opcode::HaltReturn;
+  std::string target;
+  std::vector<Operand> operands;
+  std::vector<std::size_t> jump_targets;
+};
+
 struct RationalProgram {
+  std::vector<std::string> inputs;
+  std::string output;
+  std::vector<TacInstruction> body;
+  // B200 extension: set by pipe::generate_rp (the program is that spec's
+  // emitted MWP-CWP program with `rep_mode`); null for bare programs.
   std::shared_ptr<const perf::MetricSpec> spec;
   perf::RepMode rep_mode = perf::RepMode::Real;
-  std::vector<std::string> inputs;
-  std::string output = "total_cycles";
 };
+
+// Interpreter errors (interp.hpp:19-29) and ratprog::DivisionByZero
+// (rational.hpp:20-24), raised from the GPU evaluation of bare programs.
+struct EvalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StepLimitExceeded : EvalError {
+  using EvalError::EvalError;
+};
+struct MissingBinding : EvalError {
+  using EvalError::EvalError;
+};
+
+struct ParseError : std::runtime_error {
+  std::size_t line, column;
+  ParseError(std::size_t l, std::size_t c, const std::string& why)
+      : std::runtime_error("line " + std::to_string(l) + ", column " + std::to_string(c) + ": " +
+                           why),
+        line(l),
+        column(c) {}
+};
+
+// ir::parse (ir_text.hpp:97-240): same grammar, checks and messages.
+inline RationalProgram parse(std::string_view text) {
+  struct Tok {
+    std::string s;
+    std::size_t col;
+  };
+  auto ident = [](const std::string& s) {
+    if (s.empty() || !(std::isalpha((unsigned char)s[0]) || s[0] == '_')) return false;
+    return std::all_of(s.begin(), s.end(),
+                       [](char c) { return std::isalnum((unsigned char)c) || c == '_'; });
+  };
+  auto index_of = [](const Tok& t, std::size_t line) -> std::size_t {
+    if (t.s.empty() || !std::all_of(t.s.begin(), t.s.end(), [](char c) { return std::isdigit((unsigned char)c); }))
+      throw ParseError(line, t.col, "expected instruction index, got '" + t.s + "'");
+    return (std::size_t)std::stoull(t.s);
+  };
+  RationalProgram p;
+  int stage = 0;  // 0: expect inputs, 1: expect output, 2: body
+  std::size_t line = 0, pos = 0;
+  while (pos <= text.size()) {
+    std::size_t eol = text.find('\n', pos);
+    if (eol == std::string_view::npos) eol = text.size();
+    const std::string_view raw = text.substr(pos, eol - pos);
+    pos = eol + 1;
+    ++line;
+    std::vector<Tok> toks;
+    for (std::size_t i = 0; i < raw.size();) {
+      const char c = raw[i];
+      if (c == '#') break;
+      if (c == ' ' || c == '\t') {
+        ++i;
+        continue;
+      }
+      std::size_t j = i;
+      while (j < raw.size() && raw[j] != ' ' && raw[j] != '\t' && raw[j] != '#') ++j;
+      toks.push_back({std::string(raw.substr(i, j - i)), i + 1});
+      i = j;
+    }
+    if (toks.empty()) {
+      if (eol == text.size()) break;
+      continue;
+    }
+    if (stage == 0) {
+      if (toks[0].s != "inputs:") throw ParseError(line, toks[0].col, "expected 'inputs:' header");
+      for (std::size_t i = 1; i < toks.size(); ++i) {
+        if (!ident(toks[i].s)) throw ParseError(line, toks[i].col, "bad input name '" + toks[i].s + "'");
+        p.inputs.push_back(toks[i].s);
+      }
+      stage = 1;
+    } else if (stage == 1) {
+      if (toks[0].s != "output:" || toks.size() != 2 || !ident(toks[1].s))
+        throw ParseError(line, toks[0].col, "expected 'output: <variable>' header");
+      p.output = toks[1].s;
+      stage = 2;
+    } else {
+      const Tok& head = toks[0];
+      if (head.s.back() != ':') throw ParseError(line, head.col, "expected '<index>:'");
+      const std::size_t idx = index_of(Tok{head.s.substr(0, head.s.size() - 1), head.col}, line);
+      if (idx != p.body.size())
+        throw ParseError(line, head.col, "instruction index " + std::to_string(idx) +
+                                             " out of order; expected " + std::to_string(p.body.size()));
+      if (toks.size() < 2) throw ParseError(line, head.col, "missing opcode");
+      TacInstruction ins;
+      int code = 0;
+      while (code < 14 && toks[1].s != opcode_name(static_cast<Opcode>(code))) ++code;
+      if (code == 14) throw ParseError(line, toks[1].col, "unknown opcode '" + toks[1].s + "'");
+      ins.op = static_cast<Opcode>(code);
+      std::vector<Tok> args, targets;
+      bool arrow = false;
+      for (std::size_t i = 2; i < toks.size(); ++i) {
+        if (toks[i].s == "->") {
+          if (arrow) throw ParseError(line, toks[i].col, "duplicate '->'");
+          arrow = true;
+        } else {
+          (arrow ? targets : args).push_back(toks[i]);
+        }
+      }
+      // (operands incl. target variable, jump targets, has target variable)
+      std::size_t na = 3, nt = 0;
+      bool tv = true;
+      switch (ins.op) {
+        case Opcode::Assign: case Opcode::Neg: na = 2; break;
+        case Opcode::BranchIf: na = 1; nt = 2; tv = false; break;
+        case Opcode::Jump: na = 0; nt = 1; tv = false; break;
+        case Opcode::HaltReturn: na = 1; tv = false; break;
+        default: break;
+      }
+      const std::string opn = opcode_name(ins.op);
+      if (args.size() != na)
+        throw ParseError(line, toks[1].col, opn + " expects " + std::to_string(na) +
+                                                " argument(s), got " + std::to_string(args.size()));
+      if (targets.size() != nt)
+        throw ParseError(line, toks[1].col, opn + " expects " + std::to_string(nt) +
+                                                " jump target(s), got " + std::to_string(targets.size()));
+      std::size_t a0 = 0;
+      if (tv) {
+        if (!ident(args[0].s)) throw ParseError(line, args[0].col, "bad target variable '" + args[0].s + "'");
+        ins.target = args[0].s;
+        a0 = 1;
+      }
+      for (std::size_t i = a0; i < args.size(); ++i) {
+        if (ident(args[i].s)) {
+          ins.operands.push_back(var(args[i].s));
+        } else if (args[i].s.find('.') != std::string::npos) {
+          throw ParseError(line, args[i].col, "decimal literals are not part of the format; use num/den");
+        } else {
+          try {
+            ins.operands.push_back(lit(parse_rational(args[i].s)));
+          } catch (const std::invalid_argument& e) {
+            throw ParseError(line, args[i].col, e.what());
+          }
+        }
+      }
+      for (const Tok& t : targets) ins.jump_targets.push_back(index_of(t, line));
+      p.body.push_back(std::move(ins));
+    }
+    if (eol == text.size()) break;
+  }
+  if (stage == 0) throw ParseError(line + 1, 1, "missing 'inputs:' header");
+  if (stage == 1) throw ParseError(line + 1, 1, "missing 'output:' header");
+  if (p.body.empty()) throw ParseError(line + 1, 1, "empty program body");
+  return p;
+}
+
 }  // namespace ir
 
 namespace pipe {
@@ -908,6 +1289,7 @@ inline ir::RationalProgram generate_rp(const MetricModelSet& models, const perf:
   rp.spec = std::make_shared<perf::MetricSpec>(to_metric_spec(models));
   rp.rep_mode = opts.rep_mode;
   rp.inputs = rp.spec->variables;
+  rp.output = "total_cycles";
   return rp;
 }
 
@@ -1151,13 +1533,124 @@ inline SearchResult search_optimal(const perf::MetricSpec& spec,
                                    const std::vector<long long>& data_params,
                                    const perf::DeviceProfile& hw,
                                    const std::vector<perf::LaunchConfig>& space,
-                                   const SearchOptions& opts = {}) {
-  if (space.empty()) throw std::invalid_argument("search_optimal: configuration space is empty");
-  Plan plan(spec, hw, space, opts);
-  std::vector<double> ec;
-  std::vector<uint8_t> tag;
-  std::vector<int32_t> wocc;
-  plan.evaluate(data_params, &ec, &tag, &wocc);
+                                   const SearchOptions& opts = {});
+
+namespace detail {
+
+// A bare ir::RationalProgram lowered to include/rpg.h's rpg_program: one slot
+// per variable (inputs first), literals as their correctly rounded doubles,
+// inputs bound as make_binding_plan binds them (pipeline.hpp:482-516) —
+// bx/by/bz per configuration, D<k> from the data tuple, profile fields fixed.
+struct LoweredProgram {
+  rpg_program prog{};
+  std::vector<rpg_instr> body;
+  std::vector<double> lits;
+  std::vector<int32_t> islot, ikind;
+  std::vector<double> ifixed;
+  std::vector<std::string> slot_names;
+
+  LoweredProgram(const ir::RationalProgram& rp, const std::vector<long long>& data_params,
+                 const perf::DeviceProfile& hw, std::size_t step_limit) {
+    std::map<std::string, int32_t> slots;
+    auto slot = [&](const std::string& name) {
+      auto it = slots.find(name);
+      if (it != slots.end()) return it->second;
+      const int32_t k = (int32_t)slot_names.size();
+      slots.emplace(name, k);
+      slot_names.push_back(name);
+      return k;
+    };
+    for (const std::string& in : rp.inputs) slot(in);
+    std::map<std::string, int32_t> lit_index;
+    auto operand = [&](const ir::Operand& o) -> int32_t {
+      if (o.is_var()) return slot(o.var);
+      const std::string key = (o.lit.negative ? "-" : "") + o.lit.num + "/" + o.lit.den;
+      auto it = lit_index.find(key);
+      if (it == lit_index.end()) {
+        it = lit_index.emplace(key, (int32_t)lits.size()).first;
+        lits.push_back(to_double(o.lit));
+      }
+      return -1 - it->second;
+    };
+    for (const ir::TacInstruction& ins : rp.body) {
+      rpg_instr r{};
+      r.op = static_cast<int32_t>(ins.op);
+      r.target = ins.target.empty() ? -1 : slot(ins.target);
+      if (ins.operands.size() > 0) r.a = operand(ins.operands[0]);
+      if (ins.operands.size() > 1) r.b = operand(ins.operands[1]);
+      if (ins.jump_targets.size() > 0) r.t0 = (int32_t)ins.jump_targets[0];
+      if (ins.jump_targets.size() > 1) r.t1 = (int32_t)ins.jump_targets[1];
+      body.push_back(r);
+    }
+    const int32_t out_slot = slot(rp.output);
+    const rpg_profile p = to_rpg(hw);
+    const std::map<std::string, double> fixed = {
+        {"R_max", (double)p.R_max}, {"Z_max", (double)p.Z_max}, {"T_max", (double)p.T_max},
+        {"B_max", (double)p.B_max}, {"W_max", (double)p.W_max}, {"num_SM", (double)p.num_SM},
+        {"freq_GHz", p.freq_GHz}, {"mem_latency_cycles", p.mem_latency_cycles},
+        {"departure_del_coal_cycles", p.departure_del_coal_cycles},
+        {"departure_del_uncoal_cycles", p.departure_del_uncoal_cycles},
+        {"mem_bandwidth_GBps", p.mem_bandwidth_GBps}, {"issue_cycles", p.issue_cycles},
+        {"load_bytes_per_warp", (double)p.load_bytes_per_warp},
+        {"uncoal_per_mw", (double)p.uncoal_per_mw}};
+    for (const std::string& in : rp.inputs) {
+      islot.push_back(slots.at(in));
+      int32_t kind = RPG_INPUT_FIXED;
+      double value = 0.0;
+      if (in == "bx" || in == "by" || in == "bz") {
+        kind = in == "bx" ? RPG_VAR_BX : in == "by" ? RPG_VAR_BY : RPG_VAR_BZ;
+      } else if (auto f = fixed.find(in); f != fixed.end()) {
+        value = f->second;
+      } else if (in.size() >= 2 && in[0] == 'D' &&
+                 in.find_first_not_of("0123456789", 1) == std::string::npos) {
+        const unsigned long k = std::stoul(in.substr(1));
+        if (k < 1 || k > data_params.size())
+          throw PipelineError("program input '" + in + "' has no value: " +
+                              std::to_string(data_params.size()) + " data parameter(s) were given");
+        kind = (int32_t)(k - 1);
+      } else {
+        throw PipelineError("program input '" + in +
+                            "' is neither a block dimension, a data parameter, nor a device "
+                            "profile field");
+      }
+      ikind.push_back(kind);
+      ifixed.push_back(value);
+    }
+    if (lits.empty()) lits.push_back(0.0);
+    prog.n_instr = (int32_t)body.size();
+    prog.n_slots = (int32_t)slot_names.size();
+    prog.n_literals = (int32_t)lit_index.size();
+    prog.output_slot = out_slot;
+    prog.body = body.data();
+    prog.literals = lits.data();
+    prog.n_inputs = (int32_t)rp.inputs.size();
+    prog.input_slot = islot.data();
+    prog.input_kind = ikind.data();
+    prog.input_fixed = ifixed.data();
+    prog.step_limit = (int64_t)step_limit;
+  }
+
+  // RPG_E_EVAL message -> the interpreter's exception (interp.hpp:19-121).
+  [[noreturn]] void rethrow_eval(const std::string& msg) const {
+    const std::string pre = "no value bound for variable slot ";
+    if (msg.rfind(pre, 0) == 0) {
+      size_t end = pre.size();
+      while (end < msg.size() && std::isdigit((unsigned char)msg[end])) ++end;
+      const size_t k = std::stoul(msg.substr(pre.size(), end - pre.size()));
+      throw ir::MissingBinding("no value bound for variable '" +
+                               (k < slot_names.size() ? slot_names[k] : msg) + "'" + msg.substr(end));
+    }
+    if (msg.find("zero divisor") != std::string::npos) throw DivisionByZero(msg);
+    if (msg.rfind("step limit", 0) == 0) throw ir::StepLimitExceeded(msg);
+    throw ir::EvalError(msg);
+  }
+};
+
+// search_optimal's ranking (pipeline.hpp:612-680) over per-configuration
+// program values, occupancies and tags.
+inline SearchResult rank_rows(const std::vector<perf::LaunchConfig>& space,
+                              const std::vector<double>& ec, const std::vector<double>& occ,
+                              const std::vector<std::string>& tags, double tie_rel_tol) {
   const size_t n = space.size();
   std::vector<size_t> feasible;
   for (size_t i = 0; i < n; ++i)
@@ -1171,37 +1664,166 @@ inline SearchResult search_optimal(const perf::MetricSpec& spec,
     return a < b;
   });
   const double best = ec[feasible.front()];
-  const double bound = best + best * opts.tie_rel_tol;
+  const double bound = best + best * tie_rel_tol;
   size_t ties = 0;
   while (ties < feasible.size() && ec[feasible[ties]] <= bound) ++ties;
   std::stable_sort(feasible.begin(), feasible.begin() + ties,
-                   [&](size_t a, size_t b) { return wocc[a] > wocc[b]; });
+                   [&](size_t a, size_t b) { return occ[a] > occ[b]; });
   SearchResult out;
   out.evaluated = n;
   out.infeasible = n - feasible.size();
   out.ties = ties;
   out.ranking.reserve(feasible.size());
-  for (size_t i : feasible)
-    out.ranking.push_back(SearchRow{space[i], ec[i], (double)wocc[i] / (double)hw.W_max,
-                                    detail::case_label(tag[i])});
+  for (size_t i : feasible) out.ranking.push_back(SearchRow{space[i], ec[i], occ[i], tags[i]});
   return out;
 }
 
-// The reference's signature (pipeline.hpp:575-579) for programs produced by
-// generate_rp; occupancy comes from opts.metrics when given (as in the
-// reference), else from the program's own spec.
+// Occupancy from the options' regs/shared for every configuration
+// (pipeline.hpp:648-650), on the GPU direct model.
+inline std::vector<double> option_occupancy(const perf::DeviceProfile& hw,
+                                            const std::vector<perf::LaunchConfig>& space,
+                                            const SearchOptions& opts) {
+  const size_t n = space.size();
+  std::vector<double> mv(n * RPG_N_METRICS, 0.0);
+  std::vector<rpg_config> cfg(n);
+  for (size_t i = 0; i < n; ++i) {
+    mv[i * RPG_N_METRICS + RPG_METRIC_REGS] = opts.regs_per_thread;
+    mv[i * RPG_N_METRICS + RPG_METRIC_SHARED] = opts.shared_words_per_block;
+    cfg[i] = {space[i].bx, space[i].by, space[i].bz};
+  }
+  std::vector<int32_t> b(n), w(n), st(n);
+  const rpg_profile p = to_rpg(hw);
+  char err[512] = {0};
+  const int rc = rpg_mwpcwp_cycles_batch(&p, mv.data(), cfg.data(), (int64_t)n,
+                                         RPG_REP_REAL, opts.device, nullptr, b.data(), w.data(),
+                                         nullptr, st.data(), err, sizeof err);
+  if (rc != RPG_OK) rethrow(rc, err);
+  std::vector<double> occ(n);
+  for (size_t i = 0; i < n; ++i) occ[i] = (double)w[i] / (double)hw.W_max;
+  return occ;
+}
+
+// Occupancy and case tag of every configuration under a metric spec: the
+// direct-path diagnostics search_optimal computes with opts.metrics
+// (pipeline.hpp:629-647, incl. the DenominatorNearZero fallback).
+inline void spec_diagnostics(const perf::MetricSpec& spec, const std::vector<long long>& data_params,
+                             const perf::DeviceProfile& hw,
+                             const std::vector<perf::LaunchConfig>& space,
+                             const SearchOptions& opts, std::vector<double>* occ,
+                             std::vector<std::string>* tags);
+
+}  // namespace detail
+
+// The reference's signature (pipeline.hpp:575-579).  For a program from
+// generate_rp, Ec is that spec's program evaluated on the GPU; for a bare
+// program (spec == nullptr), the program itself is lowered and evaluated on
+// the GPU (rpg_program_plan_create).  Diagnostics follow the reference:
+// with opts.metrics, occupancy and case tag come from that spec's direct
+// model; without it, occupancy comes from opts.regs_per_thread /
+// shared_words_per_block and the tag is "-" (pipeline.hpp:629-651).
 inline SearchResult search_optimal(const ir::RationalProgram& rp,
                                    const std::vector<long long>& data_params,
                                    const perf::DeviceProfile& hw,
                                    const std::vector<perf::LaunchConfig>& space,
                                    const SearchOptions& opts = {}) {
-  if (!rp.spec)
-    throw PipelineError("program was not generated from a metric spec; bare-program search "
-                        "is not supported by the B200 path yet");
-  SearchOptions o = opts;
-  o.rep_mode = rp.rep_mode;
-  return search_optimal(opts.metrics ? *opts.metrics : *rp.spec, data_params, hw, space, o);
+  if (space.empty()) throw std::invalid_argument("search_optimal: configuration space is empty");
+  if (rp.spec) {
+    SearchOptions o = opts;
+    o.rep_mode = rp.rep_mode;
+    if (opts.metrics == rp.spec.get() ||
+        (opts.metrics && opts.metrics->variables == rp.spec->variables &&
+         opts.metrics->constants == rp.spec->constants &&
+         opts.metrics->models.size() == rp.spec->models.size() &&
+         std::equal(opts.metrics->models.begin(), opts.metrics->models.end(),
+                    rp.spec->models.begin(), [](const auto& x, const auto& y) {
+                      return x.first == y.first && x.second.num.coeffs == y.second.num.coeffs &&
+                             x.second.den.coeffs == y.second.den.coeffs &&
+                             x.second.num.basis == y.second.num.basis &&
+                             x.second.den.basis == y.second.den.basis;
+                    })))
+      return search_optimal(*rp.spec, data_params, hw, space, o);
+    Plan plan(*rp.spec, hw, space, o);
+    std::vector<double> ec;
+    std::vector<uint8_t> tag;
+    std::vector<int32_t> wocc;
+    plan.evaluate(data_params, &ec, &tag, &wocc);
+    std::vector<double> occ;
+    std::vector<std::string> tags(space.size(), "-");
+    if (opts.metrics) detail::spec_diagnostics(*opts.metrics, data_params, hw, space, o, &occ, &tags);
+    else occ = detail::option_occupancy(hw, space, opts);
+    return detail::rank_rows(space, ec, occ, tags, opts.tie_rel_tol);
+  }
+  detail::LoweredProgram low(rp, data_params, hw, opts.step_limit);
+  std::vector<rpg_config> cfg(space.size());
+  for (size_t i = 0; i < space.size(); ++i) cfg[i] = {space[i].bx, space[i].by, space[i].bz};
+  const rpg_profile p = detail::to_rpg(hw);
+  const rpg_options ro = detail::to_rpg(opts);
+  rpg_plan* plan = nullptr;
+  char err[1024] = {0};
+  int rc = rpg_program_plan_create(&low.prog, &p, cfg.data(), (int64_t)cfg.size(), &ro,
+                                   opts.device, &plan, err, sizeof err);
+  if (rc != RPG_OK) detail::rethrow(rc, err);
+  const size_t n = space.size();
+  std::vector<double> ec(n);
+  std::vector<uint8_t> tag(n);
+  std::vector<int32_t> wocc(n);
+  std::vector<int64_t> t(data_params.begin(), data_params.end());
+  rc = rpg_evaluate(plan, t.empty() ? nullptr : t.data(), 1, (int32_t)t.size(), ec.data(),
+                    tag.data(), wocc.data(), err, sizeof err);
+  rpg_plan_destroy(plan);
+  if (rc == RPG_E_EVAL) low.rethrow_eval(err);
+  if (rc != RPG_OK) detail::rethrow(rc, err);
+  std::vector<double> occ(n);
+  std::vector<std::string> tags(n, "-");
+  if (opts.metrics) {
+    detail::spec_diagnostics(*opts.metrics, data_params, hw, space, opts, &occ, &tags);
+  } else {
+    for (size_t i = 0; i < n; ++i) occ[i] = (double)wocc[i] / (double)hw.W_max;
+  }
+  return detail::rank_rows(space, ec, occ, tags, opts.tie_rel_tol);
 }
+
+inline SearchResult search_optimal(const perf::MetricSpec& spec,
+                                   const std::vector<long long>& data_params,
+                                   const perf::DeviceProfile& hw,
+                                   const std::vector<perf::LaunchConfig>& space,
+                                   const SearchOptions& opts) {
+  if (space.empty()) throw std::invalid_argument("search_optimal: configuration space is empty");
+  Plan plan(spec, hw, space, opts);
+  std::vector<double> ec;
+  std::vector<uint8_t> tag;
+  std::vector<int32_t> wocc;
+  plan.evaluate(data_params, &ec, &tag, &wocc);
+  std::vector<double> occ(space.size());
+  std::vector<std::string> tags(space.size());
+  for (size_t i = 0; i < space.size(); ++i) {
+    occ[i] = (double)wocc[i] / (double)hw.W_max;
+    tags[i] = detail::case_label(tag[i]);
+  }
+  return detail::rank_rows(space, ec, occ, tags, opts.tie_rel_tol);
+}
+
+namespace detail {
+inline void spec_diagnostics(const perf::MetricSpec& spec, const std::vector<long long>& data_params,
+                             const perf::DeviceProfile& hw,
+                             const std::vector<perf::LaunchConfig>& space,
+                             const SearchOptions& opts, std::vector<double>* occ,
+                             std::vector<std::string>* tags) {
+  SearchOptions o = opts;
+  o.metrics = nullptr;
+  Plan plan(spec, hw, space, o);
+  std::vector<double> ec;
+  std::vector<uint8_t> tag;
+  std::vector<int32_t> wocc;
+  plan.evaluate(data_params, &ec, &tag, &wocc);
+  occ->resize(space.size());
+  tags->resize(space.size());
+  for (size_t i = 0; i < space.size(); ++i) {
+    (*occ)[i] = (double)wocc[i] / (double)hw.W_max;
+    (*tags)[i] = case_label(tag[i]);
+  }
+}
+}  // namespace detail
 
 // Batched search: one winner per data tuple, all tuples in one launch.
 inline std::vector<Winner> search_optimal_batch(const perf::MetricSpec& spec,

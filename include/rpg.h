@@ -327,6 +327,30 @@ int rpg_mwpcwp_cycles_batch(const rpg_profile* hw, const double* metrics,
                             int32_t* w_out, uint8_t* tag_out, int32_t* status_out,
                             char* err, size_t errlen);
 
+/* perf::MwpCwpBreakdown (perfmodel.hpp:284-296), every field, plus the
+ * outcome of the call: status 0 = ok, 1 = ZeroOccupancy "configuration
+ * cannot launch (no resident block)", 2 = ModelError "metrics must be
+ * non-negative", 3 = ModelError "metrics inconsistent: uncoal + coal must
+ * equal mem_insts", 4 = ZeroOccupancy "configuration yields no resident
+ * warp" (the reference's checks in its order, perfmodel.hpp:302-320). */
+typedef struct {
+  int64_t b_active, n_active_warps;
+  double mem_cycles, comp_cycles, mwp, cwp, rep;
+  int32_t case_tag; /* RPG_CASE_* */
+  int32_t status;
+  double cycles_pre_synch, synch_cost, total_cycles;
+} rpg_breakdown;
+
+/* perf::mwpcwp_cycles (perfmodel.hpp:298-395) over n rows of
+ * perf::KernelMetrics in its field order (perfmodel.hpp:68-77: regs, shared,
+ * comp, mem, uncoal, coal, synch, total_blocks — 8 doubles per row; mem is
+ * read as given) and configurations, on the GPU.  out[n] host memory.
+ * Small calls reuse a per-device stream and staging buffers (no allocation
+ * per call). */
+int rpg_mwpcwp_breakdown_batch(const rpg_profile* hw, const double* kernel_metrics,
+                               const rpg_config* configs, int64_t n, int32_t rep_mode,
+                               int32_t device, rpg_breakdown* out, char* err, size_t errlen);
+
 /* poly::eval_ratfunc (polyfit.hpp:96-130) at m points X (m x n_vars): out =
  * p/q, status 1 where DenominatorNearZero (|q| < 1e-12 max(1, |p|)). */
 int rpg_eval_ratfunc_batch(const rpg_poly* num, const rpg_poly* den, int32_t n_vars,
@@ -386,6 +410,12 @@ int rpg_aa_to_poly(const rpg_altarr* a, double* coef, uint8_t* exps, int32_t cap
 int64_t rpg_emit_altarr_header(const rpg_poly* num, const rpg_poly* den, int32_t nvar,
                                const char* const* var_names, const char* name, char* buf,
                                size_t buflen, char* err, size_t errlen);
+
+/* Specialized-kernel module statistics of this process: NVRTC compilations
+ * and modules loaded from the persistent cubin cache (directory
+ * $RPG_CACHE_DIR, else $XDG_CACHE_HOME/rpgpu, else $HOME/.cache/rpgpu;
+ * RPG_CACHE_DIR=off disables it).  Either pointer may be NULL. */
+void rpg_jit_stats(int64_t* compiles, int64_t* disk_hits);
 
 /* One-shot convenience for FFI callers. */
 int rpg_search(const rpg_model* model, const rpg_profile* hw,

@@ -60,6 +60,14 @@ class rpg_config(C.Structure):
     _fields_ = [("bx", C.c_int64), ("by", C.c_int64), ("bz", C.c_int64)]
 
 
+# perf::MwpCwpBreakdown (perfmodel.hpp:284-296) + call status (rpg.h).
+BREAKDOWN_DTYPE = np.dtype([("b_active", "<i8"), ("n_active_warps", "<i8"),
+                            ("mem_cycles", "<f8"), ("comp_cycles", "<f8"), ("mwp", "<f8"),
+                            ("cwp", "<f8"), ("rep", "<f8"), ("case_tag", "<i4"),
+                            ("status", "<i4"), ("cycles_pre_synch", "<f8"),
+                            ("synch_cost", "<f8"), ("total_cycles", "<f8")])
+
+
 class rpg_options(C.Structure):
     _fields_ = [("rep_mode", C.c_int32), ("arith", C.c_int32),
                 ("tie_rel_tol", C.c_double), ("regs_per_thread", C.c_double),
@@ -233,6 +241,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                               C.POINTER(rpg_config), C.c_int64, C.c_int32,
                                               C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                               C.c_void_p, C.c_void_p) + errbuf),
+        "rpg_mwpcwp_breakdown_batch": (C.c_int, (C.POINTER(rpg_profile), C.POINTER(C.c_double),
+                                                 C.POINTER(rpg_config), C.c_int64, C.c_int32,
+                                                 C.c_int32, C.c_void_p) + errbuf),
         "rpg_eval_ratfunc_batch": (C.c_int, (C.POINTER(rpg_poly), C.POINTER(rpg_poly), C.c_int32,
                                              C.POINTER(C.c_double), C.c_int64, C.c_int32,
                                              C.POINTER(C.c_double), C.POINTER(C.c_int32)) + errbuf),
@@ -246,6 +257,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "rpg_emit_altarr_header": (C.c_int64, (C.POINTER(rpg_poly), C.POINTER(rpg_poly), C.c_int32,
                                                C.POINTER(C.c_char_p), C.c_char_p, C.c_char_p,
                                                C.c_size_t) + errbuf),
+        "rpg_jit_stats": (None, (C.POINTER(C.c_int64), C.POINTER(C.c_int64))),
         "rpg_search": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
                                  C.POINTER(rpg_config), C.c_int64,
                                  C.POINTER(rpg_options), C.POINTER(C.c_int64),
@@ -268,7 +280,8 @@ EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_search_batch_subsets", "rpg_search_batch_subsets_device",
                     "rpg_mwpcwp_cycles_batch", "rpg_eval_ratfunc_batch", "rpg_uniform_stream",
                     "rpg_aa_pack_degs", "rpg_aa_unpack_degs", "rpg_aa_from_poly",
-                    "rpg_aa_to_poly", "rpg_emit_altarr_header")
+                    "rpg_aa_to_poly", "rpg_emit_altarr_header", "rpg_jit_stats",
+                    "rpg_mwpcwp_breakdown_batch")
 
 
 class RpgError(RuntimeError):
@@ -281,3 +294,11 @@ def check(code: int, err) -> None:
     if code != RPG_OK:
         msg = err.value.decode(errors="replace") if err is not None else ""
         raise RpgError(code, msg)
+
+
+def jit_stats() -> Tuple[int, int]:
+    """(NVRTC compilations, on-disk cubin cache hits) of this process."""
+    lib = load_library()
+    c, h = C.c_int64(0), C.c_int64(0)
+    lib.rpg_jit_stats(C.byref(c), C.byref(h))
+    return c.value, h.value

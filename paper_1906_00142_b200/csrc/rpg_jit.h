@@ -48,6 +48,11 @@ int get_module(const rpg::Params& P, const std::vector<double>& coef,
                const std::vector<uint64_t>& exps, bool fast, int device, int min_blocks,
                int threads, Module* out, std::string* err);
 
+// Process-wide counters: NVRTC compilations and modules loaded from the
+// persistent on-disk cache ($RPG_CACHE_DIR, ~/.cache/rpgpu).
+long jit_compiles();
+long jit_disk_hits();
+
 // Same, for an already generated source.
 int get_module_src(const std::string& src, int device, int min_blocks, int threads, Module* out,
                    std::string* err);

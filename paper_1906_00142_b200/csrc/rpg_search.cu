@@ -685,6 +685,11 @@ extern "C" {
 
 const char* rpg_version(void) { return "librpgpu 0.2.0 (sm_100a; ABI 1)"; }
 
+void rpg_jit_stats(int64_t* compiles, int64_t* disk_hits) {
+  if (compiles) *compiles = rpg_jit::jit_compiles();
+  if (disk_hits) *disk_hits = rpg_jit::jit_disk_hits();
+}
+
 int rpg_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
@@ -1142,6 +1147,50 @@ __global__ void direct_cycles_kernel(const Params P, const double* __restrict__ 
   }
 }
 
+// perf::mwpcwp_cycles with the full breakdown; rows in KernelMetrics field
+// order (perfmodel.hpp:68-77).  Checks in the reference's order
+// (perfmodel.hpp:302-320).
+__global__ void breakdown_kernel(const Params P, const double* __restrict__ km,
+                                 const rpg_config* __restrict__ cfgs, int64_t n,
+                                 rpg_breakdown* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* mv = km + i * 8;
+    Metrics m;
+    m.regs = mv[0];
+    m.shared = mv[1];
+    m.comp = mv[2];
+    m.mem = mv[3];
+    m.uncoal = mv[4];
+    m.coal = mv[5];
+    m.synch = mv[6];
+    m.tb = mv[7];
+    rpg_breakdown o;
+    o.b_active = o.n_active_warps = 0;
+    o.mem_cycles = o.comp_cycles = o.mwp = o.cwp = o.rep = 0.0;
+    o.cycles_pre_synch = o.synch_cost = o.total_cycles = 0.0;
+    o.case_tag = RPG_CASE_CWP_BOUND;
+    o.status = 0;
+    const double chk = __dadd_rn(__dadd_rn(m.uncoal, m.coal), -m.mem);
+    if (fabs(chk) > __dmul_rn(1e-9, m.mem > 1.0 ? m.mem : 1.0)) {
+      o.status = 3;
+    } else if (metrics_negative(m)) {
+      o.status = 2;
+    } else {
+      const rpg_config c = cfgs[i];
+      const int64_t T = c.bx * c.by * c.bz;
+      const int64_t b = active_blocks(P.hw, m.regs, m.shared, T, false);
+      const int64_t W = b ? active_warps(P.hw, b, T) : 0;
+      o.b_active = b;
+      o.n_active_warps = W;
+      if (b == 0) o.status = 1;
+      else if (W == 0) o.status = 4;
+      else mwpcwp_breakdown(P, m, b, W, o);
+    }
+    out[i] = o;
+  }
+}
+
 // poly::eval_ratfunc (polyfit.hpp:96-130) over m points: basis-order
 // products and sums, DenominatorNearZero flagged (status 1).
 __global__ void ratfunc_kernel(const double* __restrict__ num_c, const uint8_t* __restrict__ num_e,
@@ -1178,7 +1227,82 @@ __global__ void ratfunc_kernel(const double* __restrict__ num_c, const uint8_t* 
   }
 }
 
+// Per-device context of the direct-model entry points: one stream and one
+// growing device buffer, reused across calls (a scalar perf::active_blocks
+// through the C++ shim is one H2D, one launch and one D2H — no stream
+// creation or allocation per call).  Calls on one device serialize on the
+// context's mutex.
+struct DirectCtx {
+  std::mutex mu;
+  cudaStream_t s = nullptr;
+  char* buf = nullptr;
+  size_t cap = 0;
+  int sms = 148;
+};
+
+DirectCtx* direct_ctx(int device, cudaError_t* e) {
+  static std::mutex g;
+  static std::vector<DirectCtx*> ctx;
+  std::lock_guard<std::mutex> lk(g);
+  if (device < 0) {
+    *e = cudaErrorInvalidDevice;
+    return nullptr;
+  }
+  if ((int)ctx.size() <= device) ctx.resize(device + 1, nullptr);
+  if (!ctx[device]) {
+    *e = cudaSetDevice(device);
+    if (*e != cudaSuccess) return nullptr;
+    DirectCtx* c = new DirectCtx;
+    *e = cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking);
+    if (*e != cudaSuccess) {
+      delete c;
+      return nullptr;
+    }
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    ctx[device] = c;
+  }
+  *e = cudaSuccess;
+  return ctx[device];
+}
+
 }  // namespace
+
+extern "C" int rpg_mwpcwp_breakdown_batch(const rpg_profile* hw, const double* kernel_metrics,
+                                          const rpg_config* configs, int64_t n, int32_t rep_mode,
+                                          int32_t device, rpg_breakdown* out, char* err,
+                                          size_t errlen) {
+  if (!hw || (n > 0 && (!kernel_metrics || !configs || !out)))
+    return set_err(err, errlen, RPG_E_INVALID, "rpg_mwpcwp_breakdown_batch: null argument");
+  int rc = validate_profile(hw, err, errlen);
+  if (rc) return rc;
+  if (rep_mode != RPG_REP_REAL && rep_mode != RPG_REP_CEIL)
+    return set_err(err, errlen, RPG_E_INVALID, "rep_mode must be real or ceil");
+  if (n <= 0) return RPG_OK;
+  Params P{};
+  P.hw = *hw;
+  hoist_hardware(P);
+  P.rep_mode = rep_mode;
+  cudaError_t e;
+  DirectCtx* c = direct_ctx(device, &e);
+  if (!c) return set_err(err, errlen, RPG_E_CUDA, "rpg_mwpcwp_breakdown_batch: %s", cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(c->mu);
+  CUDA_TRY(cudaSetDevice(device));
+  const size_t in_m = sizeof(double) * 8 * (size_t)n;
+  const size_t in_c = sizeof(rpg_config) * (size_t)n;
+  const size_t o_b = sizeof(rpg_breakdown) * (size_t)n;
+  CUDA_TRY(ensure(&c->buf, &c->cap, in_m + in_c + o_b));
+  double* d_m = reinterpret_cast<double*>(c->buf);
+  rpg_config* d_c = reinterpret_cast<rpg_config*>(c->buf + in_m);
+  rpg_breakdown* d_o = reinterpret_cast<rpg_breakdown*>(c->buf + in_m + in_c);
+  CUDA_TRY(cudaMemcpyAsync(d_m, kernel_metrics, in_m, cudaMemcpyHostToDevice, c->s));
+  CUDA_TRY(cudaMemcpyAsync(d_c, configs, in_c, cudaMemcpyHostToDevice, c->s));
+  const int grid = (int)std::min<int64_t>((n + 127) / 128, (int64_t)c->sms * 8);
+  breakdown_kernel<<<grid, 128, 0, c->s>>>(P, d_m, d_c, n, d_o);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(out, d_o, o_b, cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  return RPG_OK;
+}
 
 extern "C" int rpg_mwpcwp_cycles_batch(const rpg_profile* hw, const double* metrics,
                                        const rpg_config* configs, int64_t n, int32_t rep_mode,
@@ -1196,44 +1320,34 @@ extern "C" int rpg_mwpcwp_cycles_batch(const rpg_profile* hw, const double* metr
   P.hw = *hw;
   hoist_hardware(P);
   P.rep_mode = rep_mode;
+  cudaError_t e;
+  DirectCtx* c = direct_ctx(device, &e);
+  if (!c) return set_err(err, errlen, RPG_E_CUDA, "rpg_mwpcwp_cycles_batch: %s", cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(c->mu);
   CUDA_TRY(cudaSetDevice(device));
-  cudaStream_t s;
-  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  char* buf = nullptr;
   const size_t in_m = sizeof(double) * RPG_N_METRICS * (size_t)n;
   const size_t in_c = sizeof(rpg_config) * (size_t)n;
   const size_t o_t = sizeof(double) * (size_t)n, o_i = sizeof(int32_t) * (size_t)n;
-  const size_t total = in_m + in_c + o_t + 3 * o_i + (size_t)n + 64;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), total, s);
-  if (e == cudaSuccess) {
-    double* d_m = reinterpret_cast<double*>(buf);
-    rpg_config* d_c = reinterpret_cast<rpg_config*>(buf + in_m);
-    double* d_t = reinterpret_cast<double*>(buf + in_m + in_c);
-    int32_t* d_b = reinterpret_cast<int32_t*>(buf + in_m + in_c + o_t);
-    int32_t* d_w = d_b + n;
-    int32_t* d_s = d_w + n;
-    uint8_t* d_g = reinterpret_cast<uint8_t*>(d_s + n);
-    cudaMemcpyAsync(d_m, metrics, in_m, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(d_c, configs, in_c, cudaMemcpyHostToDevice, s);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
-    direct_cycles_kernel<<<grid, 256, 0, s>>>(P, d_m, d_c, n, d_t, d_b, d_w, d_g, d_s);
-    e = cudaGetLastError();
-    if (e == cudaSuccess) {
-      if (total_out) cudaMemcpyAsync(total_out, d_t, o_t, cudaMemcpyDeviceToHost, s);
-      if (b_out) cudaMemcpyAsync(b_out, d_b, o_i, cudaMemcpyDeviceToHost, s);
-      if (w_out) cudaMemcpyAsync(w_out, d_w, o_i, cudaMemcpyDeviceToHost, s);
-      if (tag_out) cudaMemcpyAsync(tag_out, d_g, (size_t)n, cudaMemcpyDeviceToHost, s);
-      cudaMemcpyAsync(status_out, d_s, o_i, cudaMemcpyDeviceToHost, s);
-      e = cudaStreamSynchronize(s);
-    }
-    cudaFreeAsync(buf, s);
-  }
-  cudaStreamSynchronize(s);
-  cudaStreamDestroy(s);
-  if (e != cudaSuccess)
-    return set_err(err, errlen, RPG_E_CUDA, "rpg_mwpcwp_cycles_batch: %s", cudaGetErrorString(e));
+  CUDA_TRY(ensure(&c->buf, &c->cap, in_m + in_c + o_t + 3 * o_i + (size_t)n + 64));
+  char* buf = c->buf;
+  double* d_m = reinterpret_cast<double*>(buf);
+  rpg_config* d_c = reinterpret_cast<rpg_config*>(buf + in_m);
+  double* d_t = reinterpret_cast<double*>(buf + in_m + in_c);
+  int32_t* d_b = reinterpret_cast<int32_t*>(buf + in_m + in_c + o_t);
+  int32_t* d_w = d_b + n;
+  int32_t* d_s = d_w + n;
+  uint8_t* d_g = reinterpret_cast<uint8_t*>(d_s + n);
+  CUDA_TRY(cudaMemcpyAsync(d_m, metrics, in_m, cudaMemcpyHostToDevice, c->s));
+  CUDA_TRY(cudaMemcpyAsync(d_c, configs, in_c, cudaMemcpyHostToDevice, c->s));
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sms * 8);
+  direct_cycles_kernel<<<grid, 256, 0, c->s>>>(P, d_m, d_c, n, d_t, d_b, d_w, d_g, d_s);
+  CUDA_TRY(cudaGetLastError());
+  if (total_out) CUDA_TRY(cudaMemcpyAsync(total_out, d_t, o_t, cudaMemcpyDeviceToHost, c->s));
+  if (b_out) CUDA_TRY(cudaMemcpyAsync(b_out, d_b, o_i, cudaMemcpyDeviceToHost, c->s));
+  if (w_out) CUDA_TRY(cudaMemcpyAsync(w_out, d_w, o_i, cudaMemcpyDeviceToHost, c->s));
+  if (tag_out) CUDA_TRY(cudaMemcpyAsync(tag_out, d_g, (size_t)n, cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaMemcpyAsync(status_out, d_s, o_i, cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
   return RPG_OK;
 }
 

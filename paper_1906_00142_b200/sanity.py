@@ -96,6 +96,31 @@ def mwpcwp_cycles_batch(hw: F.DeviceProfile, metrics: np.ndarray, configs: np.nd
     return total, b, w, tag, st
 
 
+def mwpcwp_breakdown_batch(hw: F.DeviceProfile, kernel_metrics: np.ndarray, configs: np.ndarray,
+                           rep_mode: str = "real", device: int = 0) -> np.ndarray:
+    """perf::mwpcwp_cycles per row on the GPU with the full MwpCwpBreakdown
+    (rows: KernelMetrics field order, perfmodel.hpp:68-77, mem as given).
+    Returns a BREAKDOWN_DTYPE array; `status` 0 ok, 1/4 ZeroOccupancy,
+    2/3 ModelError (rpg.h)."""
+    lib = A.load_library()
+    km = np.ascontiguousarray(kernel_metrics, dtype=np.float64).reshape(-1, 8)
+    cfg = A.config_array([tuple(int(v) for v in c) for c in configs]) if len(configs) else \
+        np.zeros(0, dtype=[("bx", "<i8"), ("by", "<i8"), ("bz", "<i8")])
+    n = len(cfg)
+    if len(km) != n:
+        raise ValueError("one metrics row per configuration")
+    out = np.zeros(n, dtype=A.BREAKDOWN_DTYPE)
+    err = C.create_string_buffer(512)
+    hws = A.profile_struct(hw)
+    rc = lib.rpg_mwpcwp_breakdown_batch(
+        C.byref(hws), A.ptr(km, C.c_double) if n else None,
+        A.ptr(cfg, A.rpg_config) if n else None, n,
+        A.RPG_REP_CEIL if rep_mode == "ceil" else A.RPG_REP_REAL, device,
+        out.ctypes.data_as(C.c_void_p), err, len(err))
+    A.check(rc, err)
+    return out
+
+
 def _label(params) -> str:
     return ",".join(str(int(p)) for p in params)
 

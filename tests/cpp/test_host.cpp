@@ -83,6 +83,50 @@ static void cpu_tests() {
   CHECK(throws_with<perf::ModelError>([&] { pipe::to_metric_spec(missing); }, perf::kMetricSynch));
 }
 
+// Bare-program text and literal lowering (ir_text.hpp, rational.hpp:109-148):
+// correctly rounded doubles (Python float(Fraction) gives the expected bits).
+static void ir_tests() {
+  const std::pair<const char*, double> lits[] = {
+      {"1/3", 0x1.5555555555555p-2},
+      {"-7/2", -0x1.cp+1},
+      {"123456789012345678901234567890123456789/1000000000000000000000000000000000000000",
+       0x1.f9add3746f65fp-4},
+      {"9007199254740993", 0x1p+53},
+      {"9007199254740995/1", 0x1.0000000000002p+53},
+      {"1/10", 0x1.999999999999ap-4},
+      {"333333333333333333333333333333333333333333/999999999999999999999999999999999999999999999",
+       0x1.5d867c3ece2a5p-12},
+      {"2.5", 0x1.4p+1},
+      {"-0.125", -0x1p-3},
+      {"12345678901234567890123456789", 0x1.3f20d99235f65p+93},
+      {"0/5", 0.0}};
+  for (const auto& [text, want] : lits) CHECK(to_double(parse_rational(text)) == want);
+  CHECK(throws_with<std::invalid_argument>([] { parse_rational("3/0"); }, "zero denominator"));
+  CHECK(throws_with<std::invalid_argument>([] { parse_rational("3x"); }, "trailing characters"));
+  const char* text =
+      "# comment\n"
+      "inputs: D1 bx by issue_cycles\n"
+      "output: y\n"
+      "0: mul t D1 bx   # trailing comment\n"
+      "1: cmp_lt c t 4096\n"
+      "2: branch_if c -> 3 5\n"
+      "3: floor_div y t 7/2\n"
+      "4: jump -> 6\n"
+      "5: neg y 1\n"
+      "6: halt_return y\n";
+  ir::RationalProgram p = ir::parse(text);
+  CHECK(p.inputs.size() == 4 && p.output == "y" && p.body.size() == 7);
+  CHECK(p.body[2].op == ir::Opcode::BranchIf && p.body[2].jump_targets == (std::vector<size_t>{3, 5}));
+  CHECK(p.body[3].operands[1].lit == Rational(7, 2));
+  CHECK(throws_with<ir::ParseError>([] { ir::parse("inputs: a\noutput: y\n0: frob y a\n"); },
+                                    "line 3, column 4: unknown opcode 'frob'"));
+  CHECK(throws_with<ir::ParseError>([] { ir::parse("inputs: a\noutput: y\n1: neg y a\n"); },
+                                    "out of order; expected 0"));
+  CHECK(throws_with<ir::ParseError>([] { ir::parse("inputs: a\noutput: y\n0: add y a 1.5\n"); },
+                                    "decimal literals"));
+  CHECK(throws_with<ir::ParseError>([] { ir::parse("inputs: a\noutput: y\n"); }, "empty program body"));
+}
+
 static rpg_profile prof(const perf::DeviceProfile& hw) { return pipe::detail::to_rpg(hw); }
 
 static void gpu_tests() {
@@ -153,6 +197,26 @@ static void gpu_tests() {
   for (auto& kv : s2.models) kv.second.num.variables = kv.second.den.variables = s2.variables;
   CHECK(throws_with<pipe::PipelineError>([&] { pipe::search_optimal(s2, {64}, sample, space); }, "D2"));
 
+  // Program from generate_rp without opts.metrics: Ec from the program,
+  // occupancy from opts regs/shared, tag "-" (pipeline.hpp:648-650).
+  {
+    pipe::SearchOptions o2;
+    o2.regs_per_thread = 64;
+    pipe::SearchResult r = pipe::search_optimal(rp, {2048}, sample, space, o2);
+    pipe::SearchResult full = pipe::search_optimal(rp, {2048}, sample, space, opts);
+    CHECK(r.evaluated == full.evaluated && r.infeasible == full.infeasible);
+    for (const auto& row : r.ranking) {
+      CHECK(row.case_tag == "-");
+      CHECK(row.occupancy == perf::occupancy(sample, 64, 0, row.config.threads()));
+    }
+    std::vector<double> a, b;
+    for (const auto& row : r.ranking) a.push_back(row.estimated_cycles);
+    for (const auto& row : full.ranking) b.push_back(row.estimated_cycles);
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    CHECK(a == b);
+  }
+
   // Direct model on the GPU: the reference's known answers
   // (test_perfmodel.cpp:228-290, 373-377).
   perf::DeviceProfile sh = perf::load_profile(root + "/data/sample_device.profile");
@@ -168,20 +232,75 @@ static void gpu_tests() {
   oh.freq_GHz = 1; oh.mem_latency_cycles = 300; oh.departure_del_coal_cycles = 150;
   oh.departure_del_uncoal_cycles = 50; oh.mem_bandwidth_GBps = 2; oh.issue_cycles = 4;
   oh.load_bytes_per_warp = 100; oh.uncoal_per_mw = 5;
-  perf::KernelMetrics km;
-  km.comp_insts_per_thread = 18; km.uncoal_mem_insts_per_thread = 1; km.coal_mem_insts_per_thread = 1;
-  km.mem_insts_per_thread = 2; km.synch_insts_per_block = 0; km.total_blocks = 4;
-  auto br = perf::mwpcwp_cycles(oh, km, perf::LaunchConfig{32, 1, 1});
+  // Full MwpCwpBreakdown KATs (test_perfmodel.cpp:253-396).
+  auto mk = [](double comp, double unc, double coal, double synch, double blocks) {
+    perf::KernelMetrics k;
+    k.comp_insts_per_thread = comp; k.uncoal_mem_insts_per_thread = unc;
+    k.coal_mem_insts_per_thread = coal; k.mem_insts_per_thread = unc + coal;
+    k.synch_insts_per_block = synch; k.total_blocks = blocks;
+    return k;
+  };
+  const perf::LaunchConfig c32{32, 1, 1};
+  perf::KernelMetrics km = mk(18, 1, 1, 0, 4);
+  auto br = perf::mwpcwp_cycles(oh, km, c32);  // cwp-bound oracle
   CHECK(br.b_active == 4 && br.n_active_warps == 4);
-  CHECK(br.case_tag == perf::CaseTag::CwpBound && br.total_cycles == 1640.0);
-  perf::KernelMetrics bad = km;
+  CHECK(br.mem_cycles == 800.0 && br.comp_cycles == 80.0);
+  CHECK(br.mwp == 2.0 && br.cwp == 4.0 && br.rep == 1.0);
+  CHECK(br.case_tag == perf::CaseTag::CwpBound);
+  CHECK(br.cycles_pre_synch == 1640.0 && br.synch_cost == 0.0 && br.total_cycles == 1640.0);
+  {  // both-saturated oracle
+    perf::DeviceProfile h = oh;
+    h.B_max = 2; h.departure_del_coal_cycles = 50;
+    auto r = perf::mwpcwp_cycles(h, mk(23, 0, 2, 3, 2), c32);
+    CHECK(r.b_active == 2 && r.n_active_warps == 2);
+    CHECK(r.mem_cycles == 600.0 && r.comp_cycles == 100.0 && r.mwp == 2.0 && r.cwp == 2.0);
+    CHECK(r.case_tag == perf::CaseTag::BothSaturated);
+    CHECK(r.cycles_pre_synch == 750.0 && r.synch_cost == 300.0 && r.total_cycles == 1050.0);
+  }
+  {  // mwp-bound oracle
+    perf::DeviceProfile h = oh;
+    h.B_max = 8; h.num_SM = 2; h.departure_del_coal_cycles = 75; h.mem_bandwidth_GBps = 4;
+    auto r = perf::mwpcwp_cycles(h, mk(98, 0, 2, 0, 16), c32);
+    CHECK(r.b_active == 8 && r.n_active_warps == 8);
+    CHECK(r.mem_cycles == 600.0 && r.comp_cycles == 400.0 && r.mwp == 4.0 && r.cwp == 2.5);
+    CHECK(r.rep == 1.0 && r.case_tag == perf::CaseTag::MwpBound && r.total_cycles == 3500.0);
+    // raw latency, not the weighted one (test_perfmodel.cpp:313-332)
+    h.departure_del_coal_cycles = 30; h.departure_del_uncoal_cycles = 30;
+    auto r2 = perf::mwpcwp_cycles(h, mk(98, 1, 1, 0, 16), c32);
+    CHECK(r2.mwp == 4.0 && r2.case_tag == perf::CaseTag::MwpBound && r2.total_cycles == 3500.0);
+  }
+  {  // compute-only (test_perfmodel.cpp:334-353)
+    auto r = perf::mwpcwp_cycles(oh, mk(50, 0, 0, 2, 4), c32);
+    CHECK(r.b_active == 4 && r.n_active_warps == 4 && r.mem_cycles == 0.0 && r.comp_cycles == 200.0);
+    CHECK(r.mwp == 4.0 && r.case_tag == perf::CaseTag::CwpBound);
+    CHECK(r.cycles_pre_synch == 200.0 && r.synch_cost == 150.0 * 3 * 2 * 4);
+    CHECK(r.total_cycles == 200.0 + 3600.0);
+    CHECK(perf::mwpcwp_cycles(oh, mk(50, 0, 0, 0, 4), c32).total_cycles == 200.0);
+  }
+  {  // repetition count (test_perfmodel.cpp:385-396)
+    auto real = perf::mwpcwp_cycles(oh, mk(50, 0, 0, 0, 5), c32, perf::RepMode::Real);
+    CHECK(real.rep == 1.25 && real.total_cycles == 250.0);
+    auto ceil = perf::mwpcwp_cycles(oh, mk(50, 0, 0, 0, 5), c32, perf::RepMode::Ceil);
+    CHECK(ceil.rep == 2.0 && ceil.total_cycles == 400.0);
+  }
+  // rejections (test_perfmodel.cpp:355-383)
+  perf::KernelMetrics bad = mk(10, 1, 1, 0, 4);
   bad.mem_insts_per_thread = 3;
-  CHECK(throws_with<perf::ModelError>([&] { perf::mwpcwp_cycles(oh, bad, perf::LaunchConfig{32, 1, 1}); },
+  CHECK(throws_with<perf::ModelError>([&] { perf::mwpcwp_cycles(oh, bad, c32); },
                                       "metrics inconsistent"));
+  perf::KernelMetrics neg = mk(10, 1, 1, 0, 4);
+  neg.comp_insts_per_thread = -1;
+  CHECK(throws_with<perf::ModelError>([&] { perf::mwpcwp_cycles(oh, neg, c32); }, "non-negative"));
+  CHECK(throws_with<perf::ZeroOccupancy>(
+      [&] { perf::mwpcwp_cycles(oh, mk(10, 1, 1, 0, 4), perf::LaunchConfig{64, 32, 1}); },
+      "no resident block"));
   perf::DeviceProfile oh1 = oh;
   oh1.B_max = 1;
   CHECK(throws_with<perf::ZeroOccupancy>([&] { perf::mwpcwp_cycles(oh1, km, perf::LaunchConfig{8, 1, 1}); },
-                                         "no resident"));
+                                         "no resident warp"));
+  perf::KernelMetrics heavy = mk(10, 1, 1, 0, 4);
+  heavy.regs_per_thread = 1e9;
+  CHECK(throws_with<perf::ZeroOccupancy>([&] { perf::mwpcwp_cycles(oh, heavy, c32); }, "no resident"));
 
   // The fit on the GPU: an exact rational ground truth is recovered
   // (test_polyfit.cpp:142-228 criterion: coefficients up to scale, < 1e-8).
@@ -232,7 +351,10 @@ static void gpu_tests() {
 int main(int argc, char** argv) {
   root = argc > 2 ? argv[2] : ".";
   const std::string mode = argc > 1 ? argv[1] : "cpu";
-  if (mode == "cpu") cpu_tests();
+  if (mode == "cpu") {
+    cpu_tests();
+    ir_tests();
+  }
   else gpu_tests();
   if (g_fail) {
     std::cerr << g_fail << " check(s) failed\n";

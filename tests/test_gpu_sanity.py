@@ -131,6 +131,47 @@ def test_mwpcwp_cycles_batch_matches_direct_model():
                     assert w[i] == bd.n_active_warps and tag[i] == bd.case_tag
 
 
+def test_mwpcwp_breakdown_matches_direct_model():
+    """Every MwpCwpBreakdown field (perfmodel.hpp:284-296) bit-exact vs O1's
+    restatement, all three cases, compute-only rows, ceil/real, rejections."""
+    rng = np.random.default_rng(21)
+    fields = ("b_active", "n_active_warps", "mem_cycles", "comp_cycles", "mwp", "cwp", "rep",
+              "case_tag", "cycles_pre_synch", "synch_cost", "total_cycles")
+    for hw in (zoo.sample_hw(), zoo.random_hw(rng), zoo.b200_hw(), zoo.random_hw(rng)):
+        hws = A.profile_struct(hw)
+        n = 3000
+        unc = rng.choice([0.0, 0.0, 1.0, 7.5, 40.0], n)
+        coal = rng.choice([0.0, 3.0, 9.0, 0.25], n)
+        KM = np.column_stack([rng.choice([0.0, 16.0, 40.0, 255.0], n),
+                              rng.choice([0.0, 100.0, 9000.0], n),
+                              rng.choice([0.0, 1.0, 30.0, 500.0], n) * rng.uniform(0, 1, n),
+                              unc + coal, unc, coal, rng.uniform(0, 4, n), rng.uniform(1, 1e6, n)])
+        KM[:20, 2] = -1.0          # ModelError: negative
+        KM[20:40, 3] += 1.0        # ModelError: inconsistent mem
+        cfg = np.array(F.integer_configs(dims=3))[rng.integers(0, 30343, n)]
+        cfg[40:70] = [1500, 1, 1]  # ZeroOccupancy
+        for rep in ("real", "ceil"):
+            got = SN.mwpcwp_breakdown_batch(hw, KM, cfg, rep)
+            rm = A.RPG_REP_CEIL if rep == "ceil" else A.RPG_REP_REAL
+            seen = set()
+            for i in range(n):
+                m = o1.metrics(KM[i, 2], KM[i, 4], KM[i, 5], KM[i, 6], KM[i, 7], R=KM[i, 0], Z=KM[i, 1])
+                m.mem_insts_per_thread = KM[i, 3]
+                rc, bd = o1.mwpcwp_cycles(hws, m, tuple(int(v) for v in cfg[i]), rm)
+                st = int(got[i]["status"])
+                assert {0: 0, 1: 1, 4: 1, 2: 2, 3: 2}[st] == rc, i
+                if i < 20:
+                    assert st == 2
+                elif i < 40:
+                    assert st == 3
+                if rc == 0:
+                    for f in fields:
+                        g, w = got[i][f], getattr(bd, f)
+                        assert g == w or (np.isnan(g) and np.isnan(w)), (i, f, g, w)
+                    seen.add(int(bd.case_tag))
+            assert len(seen) >= 2, seen
+
+
 @pytest.mark.parametrize("kernel", ["specialized", "generic"])
 @pytest.mark.parametrize("arith", ["exact", "fast"])
 def test_subset_search_matches_search_over_the_subset(kernel, arith):

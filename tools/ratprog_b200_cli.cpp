@@ -2,7 +2,7 @@
 // ratprog_cli.cpp:277-332) on the B200 evaluator, plus `sweep`, the batched
 // form (one winner per data size over a whole N range in one launch).
 //
-//   ratprog-b200 search --models M --profile P --size N [--size N2 ...]
+//   ratprog-b200 search (--models M | --rp PROGRAM) --profile P --size N [--size N2 ...]
 //       [--format text|csv|json] [-o FILE] [--dump-jsonl FILE]
 //       [--rep-mode real|ceil] [--regs-per-thread R] [--shared-words Z]
 //       [--max-threads T] [--min-threads T] [--dims 1|2|3] [--jobs J]
@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <fstream>
 #include <iostream>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -41,7 +42,7 @@ void write_output(const std::string& path, const std::string& content) {
 }
 
 struct Args {
-  std::string cmd, models, profile, output = "-", dump_jsonl, format = "text",
+  std::string cmd, models, rp, profile, output = "-", dump_jsonl, format = "text",
                                rep_mode = "real", arith = "exact", kernel = "specialized",
                                space = "pow2";
   std::vector<long long> sizes;
@@ -66,19 +67,36 @@ pipe::SearchOptions options(const Args& a) {
 
 int do_search(const Args& a) {
   if (a.profile.empty()) return usage_error("--profile is required (or set RATPROG_PROFILE)");
-  if (a.models.empty()) return usage_error("--models is required (bare --rp programs are not supported on the B200 path)");
+  if (a.models.empty() == a.rp.empty())
+    return usage_error("exactly one of --models or --rp must be given");
   if (a.sizes.empty()) return usage_error("--size is required");
   if (a.format != "text" && a.format != "csv" && a.format != "json")
     return usage_error("--format must be text, csv, or json");
   perf::DeviceProfile hw = perf::load_profile(a.profile);
   auto space = data::enumerate_configs(a.max_threads, a.min_threads, a.dims);
   pipe::SearchOptions opts = options(a);
-  pipe::MetricModelSet models = pipe::read_models(a.models);
-  perf::MetricSpec spec = pipe::to_metric_spec(models);
-  perf::EmitOptions emit;
-  emit.rep_mode = opts.rep_mode;
-  ir::RationalProgram rp = pipe::generate_rp(models, hw, emit);
-  opts.metrics = &spec;
+  ir::RationalProgram rp;
+  perf::MetricSpec spec;
+  if (!a.models.empty()) {
+    pipe::MetricModelSet models = pipe::read_models(a.models);
+    spec = pipe::to_metric_spec(models);
+    perf::EmitOptions emit;
+    emit.rep_mode = opts.rep_mode;
+    rp = pipe::generate_rp(models, hw, emit);
+    opts.metrics = &spec;
+  } else {
+    // bare program (`--rp`, ratprog_cli.cpp:104-110, 305-307), lowered and
+    // evaluated on the GPU
+    std::ifstream in(a.rp, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open '" + a.rp + "'");
+    std::stringstream text;
+    text << in.rdbuf();
+    try {
+      rp = ir::parse(text.str());
+    } catch (const ir::ParseError& e) {
+      throw std::runtime_error(a.rp + ": " + e.what());
+    }
+  }
   pipe::SearchResult found = pipe::search_optimal(rp, a.sizes, hw, space, opts);
   std::string report = a.format == "csv"    ? pipe::format_search_csv(found)
                        : a.format == "json" ? pipe::format_search_jsonl(found)
@@ -137,6 +155,7 @@ int main(int argc, char** argv) {
         return argv[++i];
       };
       if (k == "--models") a.models = val();
+      else if (k == "--rp") a.rp = val();
       else if (k == "--profile") a.profile = val();
       else if (k == "--size") a.sizes.push_back(std::stoll(val()));
       else if (k == "-o" || k == "--output") a.output = val();
