@@ -1294,7 +1294,10 @@ inline ir::RationalProgram generate_rp(const MetricModelSet& models, const perf:
 }
 
 enum class Arith { Exact, Fast, FastCM };  // RPG_ARITH_* (rpg.h)
-enum class Kernel { Specialized, Generic };
+// Auto: the ahead-of-time generic kernel for single-tuple search_optimal
+// calls in Exact/Fast (no NVRTC on the reference CLI's one-call-per-process
+// path), the per-model specialized kernel for plans and batches.
+enum class Kernel { Auto, Specialized, Generic };
 
 // pipe::SearchOptions (pipeline.hpp:438-452) + B200 knobs.
 struct SearchOptions {
@@ -1306,7 +1309,7 @@ struct SearchOptions {
   double tie_rel_tol = 1e-12;
   std::size_t step_limit = 1000000;  // accepted for source compatibility
   Arith arith = Arith::Exact;
-  Kernel kernel = Kernel::Specialized;
+  Kernel kernel = Kernel::Auto;
   int device = 0;
 };
 
@@ -1742,6 +1745,7 @@ inline SearchResult search_optimal(const ir::RationalProgram& rp,
                              x.second.den.basis == y.second.den.basis;
                     })))
       return search_optimal(*rp.spec, data_params, hw, space, o);
+    if (o.kernel == Kernel::Auto && o.arith != Arith::FastCM) o.kernel = Kernel::Generic;
     Plan plan(*rp.spec, hw, space, o);
     std::vector<double> ec;
     std::vector<uint8_t> tag;
@@ -1789,7 +1793,9 @@ inline SearchResult search_optimal(const perf::MetricSpec& spec,
                                    const std::vector<perf::LaunchConfig>& space,
                                    const SearchOptions& opts) {
   if (space.empty()) throw std::invalid_argument("search_optimal: configuration space is empty");
-  Plan plan(spec, hw, space, opts);
+  SearchOptions o = opts;
+  if (o.kernel == Kernel::Auto && o.arith != Arith::FastCM) o.kernel = Kernel::Generic;
+  Plan plan(spec, hw, space, o);
   std::vector<double> ec;
   std::vector<uint8_t> tag;
   std::vector<int32_t> wocc;
@@ -1811,6 +1817,7 @@ inline void spec_diagnostics(const perf::MetricSpec& spec, const std::vector<lon
                              std::vector<std::string>* tags) {
   SearchOptions o = opts;
   o.metrics = nullptr;
+  if (o.kernel == Kernel::Auto && o.arith != Arith::FastCM) o.kernel = Kernel::Generic;
   Plan plan(spec, hw, space, o);
   std::vector<double> ec;
   std::vector<uint8_t> tag;

@@ -6,7 +6,7 @@
 //       [--format text|csv|json] [-o FILE] [--dump-jsonl FILE]
 //       [--rep-mode real|ceil] [--regs-per-thread R] [--shared-words Z]
 //       [--max-threads T] [--min-threads T] [--dims 1|2|3] [--jobs J]
-//       [--arith exact|fast|fastcm] [--kernel specialized|generic]
+//       [--arith exact|fast|fastcm] [--kernel auto|specialized|generic]
 //   ratprog-b200 sweep --models M --profile P --from LO --to HI
 //       [--space pow2|dense] [--dims 2|3] [-o FILE] [--arith ...]
 //
@@ -43,7 +43,7 @@ void write_output(const std::string& path, const std::string& content) {
 
 struct Args {
   std::string cmd, models, rp, profile, output = "-", dump_jsonl, format = "text",
-                               rep_mode = "real", arith = "exact", kernel = "specialized",
+                               rep_mode = "real", arith = "exact", kernel = "auto",
                                space = "pow2";
   std::vector<long long> sizes;
   long long lo = 0, hi = -1, max_threads = 1024, min_threads = 32;
@@ -61,7 +61,11 @@ pipe::SearchOptions options(const Args& a) {
   o.arith = a.arith == "fast"     ? pipe::Arith::Fast
             : a.arith == "fastcm" ? pipe::Arith::FastCM
                                   : pipe::Arith::Exact;
-  o.kernel = a.kernel == "generic" ? pipe::Kernel::Generic : pipe::Kernel::Specialized;
+  if (a.kernel != "auto" && a.kernel != "generic" && a.kernel != "specialized")
+    throw std::runtime_error("--kernel must be 'auto', 'specialized' or 'generic'");
+  o.kernel = a.kernel == "generic"       ? pipe::Kernel::Generic
+             : a.kernel == "specialized" ? pipe::Kernel::Specialized
+                                         : pipe::Kernel::Auto;
   return o;
 }
 
