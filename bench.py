@@ -5,12 +5,13 @@ Workload (BASELINE.json configs[1]): the 2DCONV + GEMM + ATAX rational
 programs (data/polybench/*.models.json — synthetic, default-bound fitted
 form, see data/polybench/make_specs.py) on the B200 device profile
 (data/b200.profile); a dense data-size sweep of 65,473 consecutive N values
-per GPU (N = 64..65,536 on one GPU) x all 7,262 integer block shapes
-bx*by <= 1024.  One step = search every (kernel, N) tuple for its best
-configuration (evaluator + per-N argmin) = 1.426e9 (N, bx, by) evaluations
-per GPU.  Multi-GPU: rank r sweeps the next 65,473 N values (weak scaling
-along the data-parameter axis) and the per-N winner records are all-gathered
-over NCCL inside the timed region.
+(N = 64..65,536) x all 7,262 integer block shapes bx*by <= 1024.  One step
+= search every (kernel, N) tuple for its best configuration (evaluator +
+per-N argmin) = 1.426e9 (N, bx, by) evaluations.  Multi-GPU: the same N
+range is split into contiguous blocks, one per rank (strong scaling along the
+data-parameter axis, the reference's static partition, pipeline.hpp:602),
+and the per-N winner records are all-gathered over NCCL inside the timed
+region.
 
 `--workload c4` times the parameter-estimation fit (configs[3]: 5 metrics x
 10^6 samples; samples/s; CPU baseline = O3 on a bounded sample) and
@@ -78,9 +79,10 @@ class Workload:
             self.kernels = KERNELS if name == "c2" else SUITE
             path = os.path.join(ROOT, "data", "polybench", "{}.models.json")
             self.space = F.integer_configs(1024, dims=2)
-            self.scaling = "weak" if name == "c2" else "strong"
+            self.scaling = "strong"   # N = 64..65536 split over the ranks (C2 and C3)
             self.describe = ("C2: 2DCONV+GEMM+ATAX rational programs (synthetic fitted-form models, default "
-                             "bounds), dense N sweep, 7262 integer (bx,by) configs, B200 profile" if name == "c2" else
+                             "bounds), N = 64..65536 every integer split over the GPUs, 7262 integer (bx,by) configs, "
+                             "B200 profile" if name == "c2" else
                              "C3: full PolyBench-GPU suite, 27 kernels (synthetic fitted-form models, default "
                              "bounds), N = 64..65536 every integer split over the GPUs, 7262 integer (bx,by)")
         self.specs = {k: F.models_to_metric_spec(F.read_models(path.format(k))) for k in self.kernels}
@@ -385,11 +387,18 @@ def gpu_arm(args):
     flops_per_launch = statistics.mean(official_flops(specs[k]) for k in wl.kernels) * n * len(space)
     achieved_tf = flops_per_launch / (kernel_ms / 1e3) / 1e12
     peak_tf, peak_src = fp64_peak_tflops()
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "search_kernel_traffic.json")
+    # Per-workload ncu evidence (null when this workload has no capture):
+    # DRAM bytes of one launch (--set full) and executed FP64 FLOPs per
+    # evaluation (instruction-mix metrics).
+    traffic = executed_flops = None
+    tfile = os.path.join(ROOT, "profiles", f"search_kernel_traffic_{wl.name}.json")
     if os.path.exists(tfile):
         with open(tfile) as f:
             traffic = json.load(f).get("bytes_per_launch")
+    mfile = os.path.join(ROOT, "profiles", f"search_kernel_mix_{wl.name}.json")
+    if os.path.exists(mfile):
+        with open(mfile) as f:
+            executed_flops = json.load(f).get("executed_flops_per_eval")
 
     # ---- end-to-end through the public C-ABI host API (pinned host buffers)
     pinned = torch.from_numpy(data_host).pin_memory()
@@ -444,6 +453,10 @@ def gpu_arm(args):
                          "frac": achieved_tf / peak_tf, "traffic": traffic,
                          "kernel": "search_kernel (fused evaluator + per-N argmin)",
                          "flops_per_eval": statistics.mean(official_flops(specs[k]) for k in wl.kernels),
+                         "flops_basis": "FLOP-equivalent: SURVEY 8(d) official F per evaluation (minimal "
+                                        "per-point work after the per-N collapse), not the FP64 FLOPs "
+                                        "the kernel executes",
+                         "executed_flops_per_eval_ncu": executed_flops,
                          "kernel_ms": kernel_ms, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "rpg_search_batch (pinned host buffers in and out)"},

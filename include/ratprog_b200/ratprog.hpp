@@ -1311,6 +1311,9 @@ struct SearchOptions {
   Arith arith = Arith::Exact;
   Kernel kernel = Kernel::Auto;
   int device = 0;
+  // search_optimal_batch on several GPUs of this process (rpg_plan_group):
+  // empty = {device}.  Winners are identical for any device list.
+  std::vector<int> devices;
 };
 
 struct SearchRow {
@@ -1832,14 +1835,64 @@ inline void spec_diagnostics(const perf::MetricSpec& spec, const std::vector<lon
 }
 }  // namespace detail
 
-// Batched search: one winner per data tuple, all tuples in one launch.
+// Batched search: one winner per data tuple, all tuples in one launch per
+// device; opts.devices lists the GPUs (contiguous tuple blocks per device,
+// rpg_search_batch_group).
 inline std::vector<Winner> search_optimal_batch(const perf::MetricSpec& spec,
                                                 const std::vector<std::vector<long long>>& tuples,
                                                 const perf::DeviceProfile& hw,
                                                 const std::vector<perf::LaunchConfig>& space,
                                                 const SearchOptions& opts = {}) {
-  Plan plan(spec, hw, space, opts);
-  return plan.search(tuples);
+  if (opts.devices.size() <= 1) {
+    SearchOptions o = opts;
+    if (!opts.devices.empty()) o.device = opts.devices[0];
+    Plan plan(spec, hw, space, o);
+    return plan.search(tuples);
+  }
+  if (space.empty()) throw std::invalid_argument("search_optimal: configuration space is empty");
+  detail::PackedModel pk(spec);
+  std::vector<rpg_config> cfg(space.size());
+  for (size_t i = 0; i < space.size(); ++i) cfg[i] = {space[i].bx, space[i].by, space[i].bz};
+  const rpg_profile p = detail::to_rpg(hw);
+  const rpg_options o = detail::to_rpg(opts);
+  std::vector<int32_t> dev(opts.devices.begin(), opts.devices.end());
+  rpg_plan_group* g = nullptr;
+  char err[1024] = {0};
+  int rc = rpg_plan_group_create(&pk.model, &p, cfg.data(), (int64_t)cfg.size(), &o, dev.data(),
+                                 (int32_t)dev.size(), &g, err, sizeof err);
+  if (rc != RPG_OK) detail::rethrow(rc, err);
+  int32_t d = 0;
+  for (const std::string& v : spec.variables)
+    if (v[0] == 'D') d = std::max(d, (int32_t)std::stoi(v.substr(1)));
+  if (!tuples.empty()) d = (int32_t)tuples.front().size();
+  std::vector<int64_t> flat;
+  for (const auto& t : tuples) {
+    if ((int32_t)t.size() != d) {
+      rpg_plan_group_destroy(g);
+      throw std::invalid_argument("data tuples differ in arity");
+    }
+    flat.insert(flat.end(), t.begin(), t.end());
+  }
+  std::vector<rpg_winner> w(tuples.size());
+  rc = rpg_search_batch_group(g, flat.data(), (int64_t)tuples.size(), d, w.data(), err, sizeof err);
+  rpg_plan_group_destroy(g);
+  if (rc != RPG_OK) detail::rethrow(rc, err);
+  std::vector<Winner> out(w.size());
+  for (size_t i = 0; i < w.size(); ++i) {
+    Winner& r = out[i];
+    r.cfg_index = w[i].cfg_idx;
+    r.feasible = (size_t)w[i].n_feasible;
+    if (w[i].cfg_idx < 0) continue;
+    r.config = space[w[i].cfg_idx];
+    r.estimated_cycles = w[i].ec;
+    r.best_cycles = w[i].best_ec;
+    r.occupancy = (double)w[i].w_occ / (double)hw.W_max;
+    r.case_tag = detail::case_label(w[i].case_tag);
+    r.ties = (size_t)w[i].ties;
+    r.b_active = w[i].b_active;
+    r.w_active = w[i].w_active;
+  }
+  return out;
 }
 
 // ---------------------------------------------------------------------------

@@ -411,6 +411,26 @@ int64_t rpg_emit_altarr_header(const rpg_poly* num, const rpg_poly* den, int32_t
                                const char* const* var_names, const char* name, char* buf,
                                size_t buflen, char* err, size_t errlen);
 
+/* ---------------------------------------------------------------------------
+ * Several GPUs behind one call (the reference parallelises search_optimal
+ * inside the call over std::threads, pipeline.hpp:595-614).  A plan group
+ * holds one plan per listed device (a device may be listed more than once).
+ * rpg_search_batch_group shards the data tuples into contiguous blocks, one
+ * per device (pipeline.hpp:602's partition); with fewer tuples than devices
+ * it splits the configuration space instead and reduces in two phases
+ * (global best Ec -> tie group -> per-device ranking of the members -> key
+ * merge), except for RPG_ARITH_FAST_CM plans, which then use the first
+ * device.  The winners are byte-identical to rpg_search_batch on one plan
+ * for any device list.  The group copies every input it needs. */
+typedef struct rpg_plan_group rpg_plan_group;
+int rpg_plan_group_create(const rpg_model* model, const rpg_profile* hw, const rpg_config* space,
+                          int64_t n_space, const rpg_options* opts, const int32_t* devices,
+                          int32_t n_devices, rpg_plan_group** out, char* err, size_t errlen);
+int rpg_plan_group_destroy(rpg_plan_group* group);
+int32_t rpg_plan_group_size(const rpg_plan_group* group);
+int rpg_search_batch_group(rpg_plan_group* group, const int64_t* data, int64_t n_tuples,
+                           int32_t d, rpg_winner* out, char* err, size_t errlen);
+
 /* Specialized-kernel module statistics of this process: NVRTC compilations
  * and modules loaded from the persistent cubin cache (directory
  * $RPG_CACHE_DIR, else $XDG_CACHE_HOME/rpgpu, else $HOME/.cache/rpgpu;

@@ -257,6 +257,14 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "rpg_emit_altarr_header": (C.c_int64, (C.POINTER(rpg_poly), C.POINTER(rpg_poly), C.c_int32,
                                                C.POINTER(C.c_char_p), C.c_char_p, C.c_char_p,
                                                C.c_size_t) + errbuf),
+        "rpg_plan_group_create": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
+                                            C.POINTER(rpg_config), C.c_int64,
+                                            C.POINTER(rpg_options), C.POINTER(C.c_int32), C.c_int32,
+                                            C.POINTER(C.c_void_p)) + errbuf),
+        "rpg_plan_group_destroy": (C.c_int, (C.c_void_p,)),
+        "rpg_plan_group_size": (C.c_int32, (C.c_void_p,)),
+        "rpg_search_batch_group": (C.c_int, (C.c_void_p, C.POINTER(C.c_int64), C.c_int64,
+                                             C.c_int32, C.c_void_p) + errbuf),
         "rpg_jit_stats": (None, (C.POINTER(C.c_int64), C.POINTER(C.c_int64))),
         "rpg_search": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
                                  C.POINTER(rpg_config), C.c_int64,
@@ -281,6 +289,8 @@ EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_mwpcwp_cycles_batch", "rpg_eval_ratfunc_batch", "rpg_uniform_stream",
                     "rpg_aa_pack_degs", "rpg_aa_unpack_degs", "rpg_aa_from_poly",
                     "rpg_aa_to_poly", "rpg_emit_altarr_header", "rpg_jit_stats",
+                    "rpg_plan_group_create", "rpg_plan_group_destroy", "rpg_plan_group_size",
+                    "rpg_search_batch_group",
                     "rpg_mwpcwp_breakdown_batch")
 
 

@@ -89,10 +89,25 @@ def sharded_fit_all_metrics(X, metric_values: Dict[str, np.ndarray], variables: 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     lo, hi = shard_range(len(order), world, rank)
-    local = G.fit_metrics(X, metric_values, variables, bounds, order[lo:hi], rank_tol, device, fit_fn)
-    gathered: List[dict] = [None] * world
+    # Any exception of the local fit (a CUDA error, an RpgError, OOM) is
+    # carried through the collective and re-raised on every rank, so no rank
+    # is left blocked in all_gather_object.
+    mine = None
+    try:
+        local = ("ok", G.fit_metrics(X, metric_values, variables, bounds, order[lo:hi], rank_tol,
+                                     device, fit_fn))
+    except Exception as e:  # noqa: BLE001 - re-raised below on every rank
+        mine = e
+        local = ("error", (rank, type(e).__name__, str(e)))
+    gathered: List[tuple] = [None] * world
     dist.all_gather_object(gathered, local, group=group)
+    for kind, payload in gathered:
+        if kind == "error":
+            r, name, msg = payload
+            if r == rank:
+                raise mine
+            raise RuntimeError(f"sharded fit failed on rank {r}: {name}: {msg}")
     outcomes: Dict[str, object] = {}
-    for part in gathered:
+    for _, part in gathered:
         outcomes.update(part)
     return G.assemble_model_set(variables, constants, outcomes)

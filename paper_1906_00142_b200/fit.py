@@ -17,6 +17,10 @@ from . import abi as A
 from . import formats as F
 
 K_DEFAULT_RANK_TOL = 1e-10
+# Largest coefficient vector (numerator + denominator basis) the GPU fit
+# handles: its R factor and Jacobi SVD live in one CTA's shared memory
+# (rpg_fit.cu kMaxCols).  Three variables at the default bounds need 35.
+K_MAX_FIT_COLUMNS = 64
 
 
 class DegenerateFit(RuntimeError):
@@ -105,6 +109,10 @@ def check_metric_inputs(X, metric_values: Dict[str, np.ndarray], variables: Sequ
         if len(nb) != len(variables) or len(db) != len(variables):
             raise F.PipelineError(f"degree bounds for metric '{metric}' must have "
                                   f"{len(variables)} entries per side")
+        cols = int(np.prod([b + 1 for b in nb])) + int(np.prod([b + 1 for b in db]))
+        if cols > K_MAX_FIT_COLUMNS:
+            raise ValueError(f"metric '{metric}': {cols} basis columns exceed the GPU fit's "
+                             f"limit of {K_MAX_FIT_COLUMNS} (lower its degree bounds)")
     return order
 
 

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import json
 import math
+import re
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -100,7 +101,7 @@ def parse_profile(text: str) -> DeviceProfile:
     for key in PROFILE_KEYS:
         v = seen[key]
         if key in _COUNT_KEYS:
-            if v != math.floor(v):
+            if not math.isfinite(v) or v != math.floor(v):
                 raise ProfileError(f"profile key '{key}' must be an integer")
             setattr(hw, key, int(v))
         else:
@@ -110,12 +111,39 @@ def parse_profile(text: str) -> DeviceProfile:
     return hw
 
 
+_STOD_DEC = re.compile(r"[+-]?(\d+\.?\d*|\.\d+)([eE][+-]?\d+)?")
+_STOD_HEX = re.compile(r"[+-]?0[xX]([0-9a-fA-F]+\.?[0-9a-fA-F]*|\.[0-9a-fA-F]+)([pP][+-]?\d+)?")
+_STOD_SPECIAL = re.compile(r"[+-]?(inf|infinity|nan(\([0-9A-Za-z_]*\))?)", re.IGNORECASE)
+
+
 def _stod(s: str) -> float:
-    # std::stod with full-consumption check: decimal/exponent forms, inf/nan
-    # spellings accepted by strtod.
-    if s == "" or s != s.strip():
+    """std::stod(s, &used) with used == s.size() (perfmodel.hpp:141-143):
+    strtod's grammar — decimal and exponent forms, hexadecimal floats
+    (0x1.8p3), inf / infinity / nan[(chars)] in any case — and stod's
+    out_of_range on overflow and on underflow of a nonzero literal.  Raises
+    ValueError on anything else (no underscores, no surrounding blanks)."""
+    if _STOD_SPECIAL.fullmatch(s):
+        return float(s.split("(")[0])
+    if _STOD_HEX.fullmatch(s):
+        sign = -1.0 if s[0] == "-" else 1.0
+        body = s.lstrip("+-")
+        if not re.search(r"[pP]", body):
+            body += "p0"
+        try:
+            v = sign * float.fromhex(body)
+        except OverflowError:
+            raise ValueError(s) from None
+        digits = re.sub(r"[pP].*$", "", body[2:])
+    elif _STOD_DEC.fullmatch(s):
+        v = float(s)
+        digits = re.sub(r"[eE].*$", "", s)
+    else:
         raise ValueError(s)
-    return float(s)
+    if math.isinf(v):
+        raise ValueError(s)  # ERANGE: overflow
+    if (v == 0.0 or abs(v) < 2.2250738585072014e-308) and re.search(r"[1-9a-fA-F]", digits):
+        raise ValueError(s)  # ERANGE: underflow of a nonzero literal
+    return v
 
 
 def load_profile(path: str) -> DeviceProfile:

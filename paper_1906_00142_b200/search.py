@@ -246,6 +246,69 @@ class Plan:
         return int(r["bx"]), int(r["by"]), int(r["bz"])
 
 
+class PlanGroup:
+    """One metric spec + profile + space resident on several GPUs of this
+    process (rpg_plan_group_*; a device may repeat).  search_batch shards
+    the tuples across the devices (or, with fewer tuples than devices, the
+    configuration space with the two-phase reduction); the winners are
+    byte-identical to Plan.search_batch on one device."""
+
+    def __init__(self, spec: F.MetricSpec, hw: F.DeviceProfile,
+                 space: Sequence[Tuple[int, int, int]], devices: Sequence[int],
+                 opts: Optional[SearchOptions] = None):
+        self.lib = A.load_library()
+        self.opts = opts or SearchOptions()
+        self.spec = spec
+        self.packed = A.PackedModel(spec)
+        self.hw_struct = A.profile_struct(hw)
+        self.space = A.config_array(list(space))
+        self.d = F.data_param_count(spec)
+        dev = np.ascontiguousarray(list(devices), dtype=np.int32)
+        self._handle = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = self.lib.rpg_plan_group_create(
+            C.byref(self.packed.struct), C.byref(self.hw_struct),
+            A.ptr(self.space, A.rpg_config) if len(self.space) else None, len(self.space),
+            C.byref(self.opts.struct()), A.ptr(dev, C.c_int32), len(dev), C.byref(self._handle),
+            err, len(err))
+        if rc != A.RPG_OK:
+            _raise(rc, err)
+
+    @property
+    def size(self) -> int:
+        return int(self.lib.rpg_plan_group_size(self._handle))
+
+    def search_batch(self, data) -> np.ndarray:
+        a = np.ascontiguousarray(data, dtype=np.int64)
+        if a.ndim == 1:
+            a = a.reshape(-1, 1) if self.d <= 1 else a.reshape(1, -1)
+        n, d = a.shape
+        out = np.zeros(n, dtype=A.WINNER_DTYPE)
+        err = C.create_string_buffer(512)
+        rc = self.lib.rpg_search_batch_group(self._handle, A.ptr(a, C.c_int64), n, d,
+                                             out.ctypes.data_as(C.c_void_p), err, len(err))
+        if rc != A.RPG_OK:
+            _raise(rc, err)
+        return out
+
+    def close(self) -> None:
+        if self._handle:
+            self.lib.rpg_plan_group_destroy(self._handle)
+            self._handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 def ranking_from_table(space: np.ndarray, ec: np.ndarray, tag: np.ndarray,
                        wocc: np.ndarray, W_max: int, tie_rel_tol: float) -> SearchResult:
     """Orders one tuple's device rows exactly as search_optimal does

@@ -160,6 +160,26 @@ static void gpu_tests() {
       }
     }
   }
+  // Several devices behind one call (device 0 listed three times here):
+  // winners identical to one device, on both axes (8 and 2 tuples).
+  {
+    auto models = pipe::read_models(root + "/data/polybench/gemm.models.json");
+    perf::MetricSpec spec = pipe::to_metric_spec(models);
+    auto space = data::integer_configs();
+    for (size_t nt : {8u, 2u}) {
+      std::vector<std::vector<long long>> tuples;
+      for (size_t i = 0; i < nt; ++i) tuples.push_back({(long long)(100 + 977 * i)});
+      pipe::SearchOptions one;
+      pipe::SearchOptions three;
+      three.devices = {0, 0, 0};
+      auto a = pipe::search_optimal_batch(spec, tuples, hw, space, one);
+      auto b = pipe::search_optimal_batch(spec, tuples, hw, space, three);
+      for (size_t i = 0; i < nt; ++i) {
+        CHECK(a[i].cfg_index == b[i].cfg_index && a[i].estimated_cycles == b[i].estimated_cycles);
+        CHECK(a[i].ties == b[i].ties && a[i].feasible == b[i].feasible && a[i].case_tag == b[i].case_tag);
+      }
+    }
+  }
   // Reference-shaped call sequence of do_search (ratprog_cli.cpp:277-332).
   perf::DeviceProfile sample = perf::load_profile(root + "/data/sample_device.profile");
   auto models = pipe::read_models(root + "/data/polybench/2dconv.models.json");

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "rpg.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|uint64_t|void|const char\*)\s+(rpg_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|uint64_t|void|const char\*)\s+(rpg_\w+)\s*\(", text, re.M)))
 
 
 def test_library_loads_and_exports_every_declared_symbol():
@@ -171,3 +171,21 @@ def test_plan_create_rejects_bad_tie_tolerance(tol):
     rc = lib.rpg_plan_create(C.byref(pk.struct), C.byref(hw), A.ptr(space, A.rpg_config), len(space),
                              C.byref(A.options_struct(tie_rel_tol=tol)), 0, C.byref(h), err, 256)
     assert rc == A.RPG_E_INVALID and b"tie_rel_tol" in err.value
+
+
+def test_profile_values_follow_stod():
+    """parse_profile's numeric values follow std::stod with a full-consumption
+    check (perfmodel.hpp:139-147): hex floats accepted, underscores and
+    out-of-range literals rejected, a non-finite count is a ProfileError."""
+    from paper_1906_00142_b200 import formats as F
+    assert F._stod("0x1.8p3") == 12.0 and F._stod("0X.8") == 0.5 and F._stod("5.") == 5.0
+    for bad in ("1_000", "1e", "0x", " 1", "1e400", "1e-400", "0x1p-1080", "1.2.3"):
+        with pytest.raises(ValueError):
+            F._stod(bad)
+    base = open(os.path.join(ROOT, "data", "sample_device.profile")).read()
+    hexed = base.replace("W_max = 48", "W_max = 0x30")
+    assert F.parse_profile(hexed).W_max == 48
+    with pytest.raises(F.ProfileError, match="bad numeric value '4_8'"):
+        F.parse_profile(base.replace("W_max = 48", "W_max = 4_8"))
+    with pytest.raises(F.ProfileError, match="'W_max' must be an integer"):
+        F.parse_profile(base.replace("W_max = 48", "W_max = inf"))

@@ -1,6 +1,5 @@
-"""bench.py host logic on CPU: the workloads' data-tuple partitions (weak
-C2, strong C3/C5 — every tuple exactly once, contiguous, equal blocks but the
-last) and the reference arm's JSON line (O1 on the host, tiny sample)."""
+"""bench.py host logic on CPU: the workloads' data-tuple partitions (strong
+C2/C3/C5 — every tuple exactly once, contiguous, equal blocks but the last) and the reference arm's JSON line (O1 on the host, tiny sample)."""
 import json
 import os
 import subprocess
@@ -15,16 +14,14 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 
-def test_c2_weak_ranges():
+def test_c2_is_configs1():
     w = bench.Workload("c2")
-    assert w.scaling == "weak" and len(w.space) == 7262 and w.kernels == ("2dconv", "gemm", "atax1")
-    for world in (1, 2, 8):
-        for r in range(world):
-            t = w.tuples(r, world)
-            assert len(t) == 65473 and t[0, 0] == 64 + r * 65473 and np.all(np.diff(t[:, 0]) == 1)
+    assert w.scaling == "strong" and len(w.space) == 7262 and w.kernels == ("2dconv", "gemm", "atax1")
+    t = w.tuples(0, 1)
+    assert len(t) == 65473 and t[0, 0] == 64 and t[-1, 0] == 65536 and np.all(np.diff(t[:, 0]) == 1)
 
 
-@pytest.mark.parametrize("name,count", [("c3", 65473), ("c5", 182 * 182)])
+@pytest.mark.parametrize("name,count", [("c2", 65473), ("c3", 65473), ("c5", 182 * 182)])
 def test_strong_partitions_cover_every_tuple_once(name, count):
     w = bench.Workload(name)
     assert w.scaling == "strong"

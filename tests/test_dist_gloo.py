@@ -156,3 +156,49 @@ def test_fit_input_checks_run_before_any_fit():
         G.check_metric_inputs(pts[:0], values, spec.variables, bounds, consts)
     with pytest.raises(G.AllMetricsFailed):
         G.assemble_model_set(spec.variables, consts, {"a": "x", "b": "y"})
+
+
+def _boom_fit(X, y, variables, nb, db, tol):
+    raise MemoryError("out of memory (simulated)")
+
+
+def _fit_error_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+    from paper_1906_00142_b200 import dist as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec, pts, values, bounds, consts = _fit_case()
+        fn = _boom_fit if rank == 1 else _o3_fit
+        try:
+            D.sharded_fit_all_metrics(pts, values, spec.variables, bounds, consts, fit_fn=fn)
+            msg = "no error"
+        except Exception as e:  # noqa: BLE001
+            msg = f"{type(e).__name__}: {e}"
+        with open(os.path.join(outdir, f"err{rank}.txt"), "w") as f:
+            f.write(msg)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_fit_error_on_one_rank_raises_on_every_rank(tmp_path):
+    """A non-numerical failure of one rank's local fit (here a simulated
+    out-of-memory) must not leave the other ranks blocked in the gather:
+    every rank raises (dist.py exception safety)."""
+    port = _free_port()
+    mp.start_processes(_fit_error_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    assert (tmp_path / "err1.txt").read_text() == "MemoryError: out of memory (simulated)"
+    assert (tmp_path / "err0.txt").read_text().startswith(
+        "RuntimeError: sharded fit failed on rank 1: MemoryError")
+
+
+def test_fit_column_limit_checked_before_any_fit():
+    from paper_1906_00142_b200 import fit as G
+    spec, pts, values, bounds, consts = _fit_case()
+    big = {k: ([2, 2, 3], [1, 1, 1]) for k in values}  # 3*3*4 + 8 = 44: fine
+    G.check_metric_inputs(pts, values, spec.variables, big, consts)
+    big = {k: ([3, 3, 3], [1, 1, 1]) for k in values}  # 64 + 8 = 72 > 64
+    with pytest.raises(ValueError, match="exceed the GPU fit's limit of 64"):
+        G.check_metric_inputs(pts, values, spec.variables, big, consts)

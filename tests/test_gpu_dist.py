@@ -146,3 +146,75 @@ def test_bench_c4_two_rank_line():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["unit"] == "samples/s"
     assert len(d["config"]["fitted"]) + len(d["config"]["failed"]) == 5 and d["config"]["fitted"]
+
+
+def _cm_worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1906_00142_b200 import formats as F
+    from paper_1906_00142_b200 import search as S
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = F.models_to_metric_spec(F.read_models(os.path.join(ROOT, "data", "polybench", "gemm.models.json")))
+        hw = F.load_profile(os.path.join(ROOT, "data", "b200.profile"))
+        data = np.arange(64, 64 + 1001, dtype=np.int64).reshape(-1, 1) * 37
+        with S.Plan(spec, hw, F.integer_configs(), S.SearchOptions(arith="fastcm")) as plan:
+            got = D.sharded_search(data, plan.search_batch)
+        np.save(os.path.join(outdir, f"rank{rank}.npy"), got.view(np.uint8))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_fastcm_search_is_rank_invariant(tmp_path):
+    """The headline arithmetic (FAST_CM) over two ranks: byte-identical to
+    one rank."""
+    from paper_1906_00142_b200 import formats as F
+    from paper_1906_00142_b200 import search as S
+    port = _free_port()
+    mp.start_processes(_cm_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    spec = F.models_to_metric_spec(F.read_models(os.path.join(ROOT, "data", "polybench", "gemm.models.json")))
+    hw = F.load_profile(os.path.join(ROOT, "data", "b200.profile"))
+    data = np.arange(64, 64 + 1001, dtype=np.int64).reshape(-1, 1) * 37
+    with S.Plan(spec, hw, F.integer_configs(), S.SearchOptions(arith="fastcm")) as plan:
+        single = plan.search_batch(data).view(np.uint8)
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"rank{r}.npy"), single)
+
+
+def test_bench_c2_two_rank_strong_scaling_line():
+    """The headline workload (C2, FAST_CM) under torch.distributed.run with
+    2 ranks on cuda:0 (gloo test mode): N = 64..65536 split over the ranks
+    (strong scaling), whole-job evaluations counted once."""
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "1", "--warmup", "3", "--no-cpu",
+           "--dist-backend", "gloo", "--same-device"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["arith"] == "fastcm"
+    assert d["config"]["evals_job_step"] == 3 * 65473 * 7262
+    assert d["config"]["tuples_rank0"] == [[64], [64 + 32736]]
+    assert d["agreement_device_vs_host_api"] is True
+
+
+@pytest.mark.skipif(__import__("torch").cuda.device_count() < 2, reason="needs 2 GPUs (NCCL)")
+def test_bench_c2_two_rank_nccl():
+    """The production multi-GPU path: one rank per GPU, NCCL all-gather of
+    the winner records inside the timed region."""
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["n_gpus"] == 2 and d["agreement_device_vs_host_api"] is True
