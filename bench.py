@@ -576,6 +576,28 @@ def c4_arm(args):
         if world > 1:
             dist.destroy_process_group()
         return 0
+    # Parity at the benchmarked arrays (untimed): each metric's GPU outcome,
+    # stage by stage, against oracle O3's committed outcome on the same
+    # arrays (tests/golden/c4_o3_noisy.json; rule in tools/fit_c4_compare.py
+    # agreement / tests/test_gpu_fit_c4.py).
+    parity = None
+    fx = os.path.join(ROOT, "tests", "golden", "c4_o3_noisy.json")
+    if os.path.exists(fx):
+        sys.path.insert(0, ROOT)
+        from tools.fit_c4_compare import agreement, holdout_points, monomials, outcome
+        with open(fx) as f:
+            o3 = json.load(f)["metrics"]
+        from paper_1906_00142_b200 import formats as F
+        Dm = monomials(F.monomial_basis([1, 1, 1]), X)
+        H = holdout_points()
+        parity = {}
+        for name in sorted(ys):
+            g = outcome(G.fit_rational, X, ys[name], var, (G.DegenerateFit, G.SvdFailure))
+            a = agreement(g, o3[name], Dm, H)
+            parity[name] = {k: a[k] for k in ("agree", "gpu_status", "o3_status", "gpu_stop", "o3_stop",
+                                              "stages_compared", "stage_max_diff", "diverged_at", "ill_posed_guard")}
+            if g["status"] == "failed":
+                parity[name]["gpu_message"] = g["message"]
     samples = len(ys) * C4_SAMPLES
     n = 35
     qr_flops = len(ys) * (2 * C4_SAMPLES * n * n - 2 * n ** 3 / 3 + 3 * C4_SAMPLES * n)
@@ -597,7 +619,8 @@ def c4_arm(args):
                                "(positivity safeguard active)", "id": "c4",
                    "api": "fit_all_metrics -> rpg_fit_rational (host buffers, H2D inside the step)"
                           + (f"; metrics sharded over {world} ranks, models all-gathered" if world > 1 else ""),
-                   "fitted": sorted(models.models), "failed": sorted(models.failures)},
+                   "fitted": sorted(models.models), "failed": sorted(models.failures),
+                   "o3_parity": parity},
         "roofline": {"bound": "fp64", "achieved": qr_flops / step_s / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": qr_flops / step_s / 1e12 / peak_tf, "traffic": None,
                      "note": "QR-equivalent FLOPs (2mn^2 - 2n^3/3 + 3mn per metric); the positivity "

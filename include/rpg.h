@@ -245,6 +245,36 @@ int rpg_fit_rational(const double* X, const double* y, int64_t m, int32_t n_vars
                      double* residual_out, int32_t* safeguard_out, char* err,
                      size_t errlen);
 
+/* rpg_fit_rational with the safeguard's intermediate results (parity
+ * diagnostics: the stages of polyfit.hpp:364-414 compared one by one with a
+ * CPU restatement).  stage_coef[0] = the unconstrained candidate (smallest
+ * right singular vector .* column scale), [1] = the first positive-
+ * denominator minimizer result, [2..] = each accepted reweighted round, all
+ * raw coordinates before make_ratfunc_from_coeffs' normalisation;
+ * round_qmin[r] = min_k q(x_k) of the vector entering reweighted round r
+ * (the guard polyfit.hpp:398); stop_reason says why the rounds ended. */
+#define RPG_FIT_TRACE_STAGES 5
+#define RPG_FIT_MAX_COLS 64
+enum {
+  RPG_FIT_STOP_NO_SAFEGUARD = -1, /* trigger not met: stage 0 is the result */
+  RPG_FIT_STOP_ROUNDS = 0,        /* all reweighted rounds ran */
+  RPG_FIT_STOP_QMIN = 1,          /* qprev.minCoeff() > 0 failed */
+  RPG_FIT_STOP_EMPTY = 2,         /* a reweighted minimizer returned empty */
+  RPG_FIT_STOP_FIRST_EMPTY = 3    /* the first minimizer returned empty */
+};
+typedef struct {
+  int32_t n_stages, stop_reason;
+  double stage_coef[RPG_FIT_TRACE_STAGES][RPG_FIT_MAX_COLS];
+  double round_qmin[RPG_FIT_TRACE_STAGES];
+} rpg_fit_trace;
+
+int rpg_fit_rational_traced(const double* X, const double* y, int64_t m, int32_t n_vars,
+                            const int32_t* num_bounds, const int32_t* den_bounds, double rank_tol,
+                            int32_t device, double* coef_out, double* sigma_out,
+                            int32_t* rank_out, int32_t* truncated_out, double* residual_out,
+                            int32_t* safeguard_out, rpg_fit_trace* trace, char* err,
+                            size_t errlen);
+
 /* A bare rational program (ir::RationalProgram, ir.hpp:19-112) lowered for
  * the GPU: variables are slots, literals are doubles (to_double of each
  * rational, as the reference's C lowering prints them, pipeline.hpp:276-433).

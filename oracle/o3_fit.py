@@ -199,8 +199,12 @@ class FitReport:
     safeguard: bool = False
 
 
-def fit_rational(X, y, variables, num_bounds, den_bounds, rank_tol=K_DEFAULT_RANK_TOL):
-    """polyfit.hpp:337-427."""
+def fit_rational(X, y, variables, num_bounds, den_bounds, rank_tol=K_DEFAULT_RANK_TOL,
+                 trace=None):
+    """polyfit.hpp:337-427.  ``trace`` (dict, optional): the safeguard's
+    stages as rpg_fit_rational_traced reports them ("stages": unconstrained
+    vector, first minimizer result, accepted reweighted rounds — raw
+    coordinates; "round_qmin"; "stop")."""
     X = np.asarray(X, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64)
     if X.ndim == 1:
@@ -214,6 +218,8 @@ def fit_rational(X, y, variables, num_bounds, den_bounds, rank_tol=K_DEFAULT_RAN
     dec = svd(A)
     cols = A.shape[1]
     c = dec.V[:, cols - 1] * col_scale
+    if trace is not None:
+        trace.update(stages=[c.copy()], round_qmin=[], stop="no_safeguard")
     den_values = eval_monomials(db, X)
     q = den_values @ c[nn:]
     sign_mixed = q.min() < 0.0 and q.max() > 0.0
@@ -230,17 +236,29 @@ def fit_rational(X, y, variables, num_bounds, den_bounds, rank_tol=K_DEFAULT_RAN
             start[:nn] += vd.V[:, i] * (uty[i] / vd.sigma[i])
         start[nn] = 1.0
         refined = positive_den_minimizer(A, col_scale, den_values, nn, start)
+        if trace is not None:
+            trace["stop"] = "rounds" if refined is not None else "first_empty"
+            if refined is not None:
+                trace["stages"].append(refined.copy())
         rnd = 0
         while refined is not None and rnd < K_REWEIGHT_ROUNDS:
             qprev = den_values @ refined[nn:]
+            if trace is not None:
+                trace["round_qmin"].append(float(qprev.min()))
             if not (qprev.min() > 0.0):
+                if trace is not None:
+                    trace["stop"] = "qmin"
                 break
             Aw = A_raw / (np.maximum(1.0, np.abs(y)) * qprev)[:, None]
             Aw, scale_w = equilibrate_columns(Aw)
             nxt = positive_den_minimizer(Aw, scale_w, den_values, nn, refined)
             if nxt is None:
+                if trace is not None:
+                    trace["stop"] = "empty"
                 break
             refined = nxt
+            if trace is not None:
+                trace["stages"].append(refined.copy())
             rnd += 1
         if refined is not None:
             c = refined

@@ -60,6 +60,17 @@ class rpg_config(C.Structure):
     _fields_ = [("bx", C.c_int64), ("by", C.c_int64), ("bz", C.c_int64)]
 
 
+RPG_FIT_TRACE_STAGES = 5
+RPG_FIT_MAX_COLS = 64
+FIT_STOP_NAMES = {-1: "no_safeguard", 0: "rounds", 1: "qmin", 2: "empty", 3: "first_empty"}
+
+
+class rpg_fit_trace(C.Structure):
+    _fields_ = [("n_stages", C.c_int32), ("stop_reason", C.c_int32),
+                ("stage_coef", (C.c_double * RPG_FIT_MAX_COLS) * RPG_FIT_TRACE_STAGES),
+                ("round_qmin", C.c_double * RPG_FIT_TRACE_STAGES)]
+
+
 # perf::MwpCwpBreakdown (perfmodel.hpp:284-296) + call status (rpg.h).
 BREAKDOWN_DTYPE = np.dtype([("b_active", "<i8"), ("n_active_warps", "<i8"),
                             ("mem_cycles", "<f8"), ("comp_cycles", "<f8"), ("mwp", "<f8"),
@@ -222,6 +233,13 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                        C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32), C.POINTER(C.c_double),
                                        C.POINTER(C.c_int32)) + errbuf),
+        "rpg_fit_rational_traced": (C.c_int, (C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                              C.c_int64, C.c_int32, C.POINTER(C.c_int32),
+                                              C.POINTER(C.c_int32), C.c_double, C.c_int32,
+                                              C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                              C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                              C.POINTER(C.c_double), C.POINTER(C.c_int32),
+                                              C.POINTER(rpg_fit_trace)) + errbuf),
         "rpg_program_plan_create": (C.c_int, (C.c_void_p, C.POINTER(rpg_profile),
                                               C.POINTER(rpg_config), C.c_int64,
                                               C.POINTER(rpg_options), C.c_int32,
@@ -290,7 +308,7 @@ EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_aa_pack_degs", "rpg_aa_unpack_degs", "rpg_aa_from_poly",
                     "rpg_aa_to_poly", "rpg_emit_altarr_header", "rpg_jit_stats",
                     "rpg_plan_group_create", "rpg_plan_group_destroy", "rpg_plan_group_size",
-                    "rpg_search_batch_group",
+                    "rpg_search_batch_group", "rpg_fit_rational_traced",
                     "rpg_mwpcwp_breakdown_batch")
 
 

@@ -41,6 +41,7 @@
 namespace rpg_fit {
 
 constexpr int kMaxCols = 64;   // n = |num basis| + |den basis|
+static_assert(kMaxCols == RPG_FIT_MAX_COLS, "rpg.h RPG_FIT_MAX_COLS");
 constexpr int kTile = 128;     // rows per SMEM tile
 constexpr int kFitThreads = 256;
 constexpr int kFitWarps = kFitThreads / 32;
@@ -1668,7 +1669,8 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
 // The positivity safeguard (polyfit.hpp:369-414).  c: in = the unconstrained
 // candidate (raw coordinates), out = the refined vector when one is found.
 int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, double* c,
-                      double rank_tol, int sms, cudaStream_t s, char* err, size_t errlen) {
+                      double rank_tol, int sms, cudaStream_t s, char* err, size_t errlen,
+                      rpg_fit_trace* trace) {
   const int nn = F0.nn, nd = F0.nd, n = F0.n;
   // The sample passes read precomputed denominator monomials.
   DevBuf dm;
@@ -1716,6 +1718,16 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
   rc = minimizer(F, R, S, gsum.as<double>(), start.as<double>(), refined.as<double>(), &found, sms,
                  s, err, errlen);
   if (rc) return rc;
+  auto record = [&](const double* dvec) -> int {
+    if (!trace || trace->n_stages >= RPG_FIT_TRACE_STAGES) return RPG_OK;
+    FCUDA(cudaMemcpyAsync(trace->stage_coef[trace->n_stages], dvec, sizeof(double) * n,
+                          cudaMemcpyDeviceToHost, s));
+    FCUDA(cudaStreamSynchronize(s));
+    ++trace->n_stages;
+    return RPG_OK;
+  };
+  if (trace) trace->stop_reason = found ? RPG_FIT_STOP_ROUNDS : RPG_FIT_STOP_FIRST_EMPTY;
+  if (found && (rc = record(refined.as<double>()))) return rc;
   FCUDA(fit_malloc((void**)&w.p, sizeof(double) * (size_t)F.m));
   FCUDA(fit_malloc((void**)&Sw.p, sizeof(double) * n));
   DevBuf cdp;
@@ -1729,7 +1741,11 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
     double qmin = 0.0;
     FCUDA(cudaMemcpyAsync(&qmin, P.out.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     FCUDA(cudaStreamSynchronize(s));
-    if (!(qmin > 0.0)) break;
+    if (trace) trace->round_qmin[round] = qmin;
+    if (!(qmin > 0.0)) {
+      if (trace) trace->stop_reason = RPG_FIT_STOP_QMIN;
+      break;
+    }
     const size_t smw = (size_t)kMaxCols * RPG_MAX_VARS + 16;
     row_weights<<<G, 256, smw, s>>>(F, cdp.as<double>(), w.as<double>());
     FitParams Fw = F;
@@ -1742,8 +1758,12 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
     rc = minimizer(F, Rwb.as<double>(), Sw.as<double>(), gsum.as<double>(), refined.as<double>(),
                    next.as<double>(), &f2, sms, s, err, errlen);
     if (rc) return rc;
-    if (!f2) break;
+    if (!f2) {
+      if (trace) trace->stop_reason = RPG_FIT_STOP_EMPTY;
+      break;
+    }
     FCUDA(cudaMemcpyAsync(refined.p, next.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    if ((rc = record(refined.as<double>()))) return rc;
   }
   if (found) FCUDA(cudaMemcpyAsync(c, refined.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   FCUDA(cudaStreamSynchronize(s));
@@ -1756,6 +1776,22 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
                                 double* sigma_out, int32_t* rank_out, int32_t* truncated_out,
                                 double* residual_out, int32_t* safeguard_out, char* err,
                                 size_t errlen) {
+  return rpg_fit_rational_traced(X, y, m, n_vars, num_bounds, den_bounds, rank_tol, device,
+                                 coef_out, sigma_out, rank_out, truncated_out, residual_out,
+                                 safeguard_out, nullptr, err, errlen);
+}
+
+extern "C" int rpg_fit_rational_traced(const double* X, const double* y, int64_t m, int32_t n_vars,
+                                       const int32_t* num_bounds, const int32_t* den_bounds,
+                                       double rank_tol, int32_t device, double* coef_out,
+                                       double* sigma_out, int32_t* rank_out,
+                                       int32_t* truncated_out, double* residual_out,
+                                       int32_t* safeguard_out, rpg_fit_trace* trace, char* err,
+                                       size_t errlen) {
+  if (trace) {
+    *trace = rpg_fit_trace{};
+    trace->stop_reason = RPG_FIT_STOP_NO_SAFEGUARD;
+  }
   if (m <= 0 || !X || !y) return fset_err(err, errlen, RPG_E_INVALID, "fit_rational: no samples");
   if (n_vars < 1 || n_vars > RPG_MAX_VARS || !num_bounds || !den_bounds)
     return fset_err(err, errlen, RPG_E_INVALID, "fit_rational: bad variable count");
@@ -1820,10 +1856,10 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
   F.exps = dexps.as<uint8_t>();
   F.m = m;
   // RPG_FIT_TRACE=1: per-phase wall times on stderr (profiling aid).
-  const bool trace = getenv("RPG_FIT_TRACE") != nullptr;
+  const bool phase_trace = getenv("RPG_FIT_TRACE") != nullptr;
   auto t_prev = std::chrono::steady_clock::now();
   auto phase = [&](const char* name) {
-    if (!trace) return;
+    if (!phase_trace) return;
     cudaStreamSynchronize(s);
     const auto now = std::chrono::steady_clock::now();
     fprintf(stderr, "[rpg_fit] %-12s %9.3f ms\n", name,
@@ -1846,6 +1882,10 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
                                         dscale.as<double>(), nullptr, 1);
   FCUDA(cudaGetLastError());
   smallest_vector<<<1, 64, 0, s>>>(dV.as<double>(), dscale.as<double>(), n, dc.as<double>());
+  if (trace) {
+    FCUDA(cudaMemcpyAsync(trace->stage_coef[0], dc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    trace->n_stages = 1;
+  }
   // Safeguard trigger statistics.
   const int G = std::max(1, std::min<int>((int)((m + 255) / 256), 4 * sms));
   FCUDA(fit_malloc((void**)&dpart.p, sizeof(double) * 4 * G));
@@ -1862,7 +1902,7 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
   phase("svd+stats");
   if (trigger) {
     rc = rpg_fit_safeguard(F, dR.as<double>(), dscale.as<double>(), dc.as<double>(), rank_tol,
-                           sms, s, err, errlen);
+                           sms, s, err, errlen, trace);
     if (rc) return rc;
     phase("safeguard");
   }

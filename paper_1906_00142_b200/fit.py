@@ -48,7 +48,11 @@ class FitReport:
 
 def fit_rational(X, y, variables: Sequence[str], num_bounds: Sequence[int],
                  den_bounds: Sequence[int], rank_tol: float = K_DEFAULT_RANK_TOL,
-                 device: int = 0) -> Tuple[F.RationalFunction, FitReport]:
+                 device: int = 0, trace: Optional[dict] = None) -> Tuple[F.RationalFunction, FitReport]:
+    """poly::fit_rational on the GPU.  ``trace`` (a dict, optional) receives
+    the safeguard's stages (rpg_fit_rational_traced): "stages" (raw
+    coefficient vectors: unconstrained, first minimizer, reweighted rounds),
+    "round_qmin" and "stop" — filled even when the fit then fails."""
     lib = A.load_library()
     X = np.ascontiguousarray(X, dtype=np.float64)
     if X.ndim == 1:
@@ -67,10 +71,17 @@ def fit_rational(X, y, variables: Sequence[str], num_bounds: Sequence[int],
     nbnd = (C.c_int32 * nv)(*num_bounds)
     dbnd = (C.c_int32 * nv)(*den_bounds)
     err = C.create_string_buffer(512)
-    rc = lib.rpg_fit_rational(A.ptr(X, C.c_double) if m else None, A.ptr(y, C.c_double) if m else None,
-                              m, nv, nbnd, dbnd, rank_tol, device, A.ptr(coef, C.c_double),
-                              A.ptr(sig, C.c_double), C.byref(rank), C.byref(trunc),
-                              C.byref(resid), C.byref(safe), err, len(err))
+    tr = A.rpg_fit_trace() if trace is not None else None
+    rc = lib.rpg_fit_rational_traced(
+        A.ptr(X, C.c_double) if m else None, A.ptr(y, C.c_double) if m else None,
+        m, nv, nbnd, dbnd, rank_tol, device, A.ptr(coef, C.c_double),
+        A.ptr(sig, C.c_double), C.byref(rank), C.byref(trunc),
+        C.byref(resid), C.byref(safe), C.byref(tr) if tr is not None else None, err, len(err))
+    if tr is not None:
+        trace["stages"] = [np.array(tr.stage_coef[i][:n]) for i in range(tr.n_stages)]
+        started = tr.n_stages - 1 + (1 if tr.stop_reason in (1, 2) else 0) if tr.n_stages >= 2 else 0
+        trace["round_qmin"] = [float(tr.round_qmin[i]) for i in range(started)]
+        trace["stop"] = A.FIT_STOP_NAMES.get(tr.stop_reason, str(tr.stop_reason))
     if rc != A.RPG_OK:
         msg = err.value.decode()
         if rc == A.RPG_E_INVALID:

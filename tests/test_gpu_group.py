@@ -25,7 +25,7 @@ def test_group_matches_single_device(arith, G):
                                rep_mode=case.rep_mode, arith=arith)
         try:
             single = S.Plan(case.spec, case.hw, case.space, opts)
-        except A.RpgError:
+        except (A.RpgError, ValueError):
             continue  # fast_cm not applicable to this model
         n_cases += 1
         with single, S.PlanGroup(case.spec, case.hw, case.space, [0] * G, opts) as grp:

@@ -84,6 +84,19 @@ def main():
     subprocess.run([sys.executable, "-c", "import sys; sys.path.insert(0, %r); "
                     "from oracle import o1; o1.lib()" % ROOT], check=True)
     out["python_o1_process_startup"] = time.perf_counter() - t0
+    probe = os.path.join(ROOT, "tools", "percall_probe")
+    if os.path.exists(probe):
+        cache2 = tempfile.mkdtemp(prefix="rpgcache")
+        env2 = dict(os.environ, RPG_CACHE_DIR=cache2)
+        out["phases_ms"] = []
+        for mode in ("generic", "specialized", "specialized", "fastcm", "fastcm"):
+            t0 = time.perf_counter()
+            r = subprocess.run([probe, MODELS, PROFILE, mode], capture_output=True, text=True, env=env2)
+            wall = time.perf_counter() - t0
+            d = json.loads(r.stdout) if r.returncode == 0 else {"error": r.stderr[-300:]}
+            d["process_wall_ms"] = 1e3 * wall
+            out["phases_ms"].append(d)
+        shutil.rmtree(cache2, ignore_errors=True)
     print(json.dumps({"metric": "cold single-call wall time (1 tuple x 51 configs)", "unit": "s",
                       "workload": "ratprog-b200 search --models gemm --size 1024", **out}))
 

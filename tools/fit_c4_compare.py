@@ -52,24 +52,48 @@ def holdout_points(n=20000, seed=77):
 
 
 def outcome(fit_fn, X, y, variables, exc):
+    """Fit outcome plus the safeguard's stages (fit_fn takes trace=dict)."""
     t0 = time.perf_counter()
+    tr = {}
     try:
-        f, rep = fit_fn(X, y, variables, [2, 2, 2], [1, 1, 1])
+        f, rep = fit_fn(X, y, variables, [2, 2, 2], [1, 1, 1], trace=tr)
     except exc as e:
-        return {"status": "failed", "message": str(e), "seconds": time.perf_counter() - t0}
+        return {"status": "failed", "message": str(e), "seconds": time.perf_counter() - t0,
+                "trace": trace_json(tr)}
     sig = [float(s) for s in rep.singular_values]
     return {"status": "fitted", "safeguard": bool(rep.safeguard), "rank": int(rep.numerical_rank),
             "truncated": bool(rep.truncated), "sigma_min": sig[-1], "sigma_1": sig[0], "sigma": sig,
             "num": [float(c) for c in f.num.coeffs], "den": [float(c) for c in f.den.coeffs],
-            "seconds": time.perf_counter() - t0}
+            "seconds": time.perf_counter() - t0, "trace": trace_json(tr)}
+
+
+def trace_json(tr):
+    return {"stages": [[float(v) for v in st] for st in tr.get("stages", [])],
+            "round_qmin": [float(q) for q in tr.get("round_qmin", [])],
+            "stop": tr.get("stop")}
+
+
+def direction(v):
+    """Unit vector of a stage, sign fixed by its largest-magnitude entry."""
+    v = np.asarray(v, dtype=float)
+    v = v / np.linalg.norm(v)
+    return v if v[np.argmax(np.abs(v))] > 0 else -v
+
+
+def stage_diffs(g, c):
+    """Per common stage: max |unit(g) - unit(c)|."""
+    sg, sc = g.get("trace", {}).get("stages", []), c.get("trace", {}).get("stages", [])
+    return [float(np.max(np.abs(direction(a) - direction(b)))) for a, b in zip(sg, sc)]
+
+
+def monomials(basis, X):
+    """Columns prod_v X[:, v] ** e_v for each exponent tuple (plain numpy)."""
+    return np.column_stack([np.prod(X ** np.asarray(e, dtype=float), axis=1) for e in basis])
 
 
 def ratfunc_values(o, X):
-    from oracle import o3_fit as O3
     nb, db = F.monomial_basis([2, 2, 2]), F.monomial_basis([1, 1, 1])
-    p = O3.eval_monomials(nb, X) @ np.array(o["num"])
-    q = O3.eval_monomials(db, X) @ np.array(o["den"])
-    return p / q
+    return (monomials(nb, X) @ np.array(o["num"])) / (monomials(db, X) @ np.array(o["den"]))
 
 
 def compare(g, c, H):
@@ -88,6 +112,58 @@ def compare(g, c, H):
     elif g["status"] == c["status"] == "failed":
         d["same_message"] = g["message"] == c["message"]
     return d
+
+
+def agreement(g, c, Dm, H, nn=27):
+    """GPU vs O3 outcome at one metric, stage by stage (the rule
+    tests/test_gpu_fit_c4.py states).  Stage s_0 is the unconstrained
+    candidate, s_1 the first positive-denominator minimizer, s_{i+1} the
+    result of reweighted round i, which weights the rows by 1 / (max(1,|y|)
+    q_i) with q_i = the denominator of s_i.  Walk the stages while both
+    agree (unit directions within 1e-6).  If the whole path agrees (same
+    stages, same stop reason) the outcomes must agree: status, safeguard,
+    rank, sigma within 1e-9 sigma_1, holdout within 1e-6.  If the paths part
+    at stage d, the stage feeding that round, s_{d-1} (d >= 2), must have a
+    denominator at rounding level of zero (min q / mean |q| < 1e-12): the
+    round's row weights reach ~1e16 there and its result — even whether it
+    runs — is undetermined for the reference algorithm itself."""
+    gs, cs = g["trace"]["stages"], c["trace"]["stages"]
+    out = {"stages_compared": 0, "stage_max_diff": 0.0, "diverged_at": None, "ill_posed_guard": None,
+           "gpu_stop": g["trace"]["stop"], "o3_stop": c["trace"]["stop"],
+           "gpu_status": g["status"], "o3_status": c["status"]}
+    rel = {}
+    d = None
+    for i in range(min(len(gs), len(cs))):
+        if i >= 1:
+            q = Dm @ np.asarray(cs[i])[nn:]
+            rel[i] = float(np.min(q) / np.mean(np.abs(q)))
+        if i == 0 and c.get("truncated"):
+            continue  # rank-deficient: the smallest singular vector is not unique
+        diff = float(np.max(np.abs(direction(gs[i]) - direction(cs[i]))))
+        if diff >= 1e-6:
+            d = i
+            break
+        out["stages_compared"] += 1
+        out["stage_max_diff"] = max(out["stage_max_diff"], diff)
+    if d is None and (len(gs) != len(cs) or out["gpu_stop"] != out["o3_stop"]):
+        d = min(len(gs), len(cs))
+    if d is None:
+        ok = g["status"] == c["status"]
+        if ok:
+            dd = compare(g, c, H)
+            out["diff"] = dd
+            if g["status"] == "fitted":
+                ok = (dd["same_safeguard"] and dd["same_rank"] and dd["sigma_max_abs_diff_over_sigma1"] < 1e-9
+                      and dd["holdout_max_rel_diff"] < 1e-6)
+            else:
+                ok = dd["same_message"]
+    else:
+        out["diverged_at"] = d
+        ok = d >= 2 and abs(rel.get(d - 1, 1.0)) < 1e-12
+        if ok:
+            out["ill_posed_guard"] = {"stage": d - 1, "min_q_over_mean_abs_q": rel[d - 1]}
+    out["agree"] = bool(ok)
+    return out
 
 
 def main():
@@ -129,6 +205,8 @@ def main():
         if c is not None:
             row["o3"] = {k: v for k, v in c.items() if k not in ("sigma",)}
             row["diff"] = compare(g, c, H)
+            row["diff"]["stage_max_abs_diff"] = stage_diffs(g, c)
+            row["diff"]["stops"] = [g.get("trace", {}).get("stop"), c.get("trace", {}).get("stop")]
         rows[name] = row
         print(name, json.dumps(row.get("diff", {})), "gpu", g["status"], g.get("safeguard"), g.get("message", ""),
               flush=True)
