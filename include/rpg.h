@@ -105,7 +105,8 @@ enum {
   RPG_E_NO_FEASIBLE = -5,  /* pipe::NoFeasibleConfig (single-tuple calls) */
   RPG_E_PIPELINE = -6,     /* pipe::PipelineError */
   RPG_E_FIT = -7,          /* poly::DegenerateFit / SvdFailure */
-  RPG_E_EVAL = -8          /* ir::EvalError / DivisionByZero (bare programs) */
+  RPG_E_EVAL = -8,         /* ir::EvalError / DivisionByZero (bare programs) */
+  RPG_E_CSV = -9           /* data::CsvError */
 };
 
 /* perf::DeviceProfile, same fields and order (perfmodel.hpp:50-65). */
@@ -274,6 +275,32 @@ int rpg_fit_rational_traced(const double* X, const double* y, int64_t m, int32_t
                             int32_t* rank_out, int32_t* truncated_out, double* residual_out,
                             int32_t* safeguard_out, rpg_fit_trace* trace, char* err,
                             size_t errlen);
+
+/* Several fits over one sample set (pipe::fit_all_metrics' loop over the
+ * metric columns, pipeline.hpp:145-184): X (m x n_vars, host) is uploaded
+ * once and the jobs run concurrently (one host thread and CUDA stream each).
+ * Per job: y (m values, host), bounds, the outputs of rpg_fit_rational
+ * (nullable) and an optional trace; status / message receive that fit's own
+ * return code and error text (RPG_E_FIT for DegenerateFit / SvdFailure).
+ * The call itself fails only on bad arguments or a failed upload. */
+typedef struct {
+  const double* y;
+  const int32_t* num_bounds;
+  const int32_t* den_bounds;
+  double* coef_out;
+  double* sigma_out;
+  int32_t* rank_out;
+  int32_t* truncated_out;
+  double* residual_out;
+  int32_t* safeguard_out;
+  rpg_fit_trace* trace;
+  int32_t status;
+  char message[252];
+} rpg_fit_job;
+
+int rpg_fit_rational_multi(const double* X, int64_t m, int32_t n_vars, rpg_fit_job* jobs,
+                           int32_t n_jobs, double rank_tol, int32_t device, char* err,
+                           size_t errlen);
 
 /* A bare rational program (ir::RationalProgram, ir.hpp:19-112) lowered for
  * the GPU: variables are slots, literals are doubles (to_double of each
@@ -460,6 +487,32 @@ int rpg_plan_group_destroy(rpg_plan_group* group);
 int32_t rpg_plan_group_size(const rpg_plan_group* group);
 int rpg_search_batch_group(rpg_plan_group* group, const int64_t* data, int64_t n_tuples,
                            int32_t d, rpg_winner* out, char* err, size_t errlen);
+
+/* ---------------------------------------------------------------------------
+ * Profiled samples at scale: data::parse_samples /
+ * format_samples (datakit.hpp:272-415) — the same CSV schema, provenance
+ * comment, checks, error precedence and CsvError messages (RPG_E_CSV) —
+ * columnar and multi-threaded (n_threads <= 0: all hardware threads).
+ * A parsed set holds n rows: data (n x d int64), configs (n x 3 int64),
+ * values (n x n_metrics float64, header order).  provenance_kind: 0 =
+ * measured, 1 = synthetic (seed, noise_rel). */
+typedef struct rpg_samples rpg_samples;
+int rpg_samples_parse(const char* text, size_t len, int32_t n_threads, rpg_samples** out,
+                      char* err, size_t errlen);
+int rpg_samples_info(const rpg_samples* s, int64_t* n_rows, int32_t* d, int32_t* n_metrics,
+                     int32_t* provenance_kind, uint64_t* seed, double* noise_rel);
+const char* rpg_samples_metric_name(const rpg_samples* s, int32_t k);
+int rpg_samples_copy(const rpg_samples* s, int64_t* data, int64_t* configs, double* values);
+void rpg_samples_free(rpg_samples* s);
+/* The CSV text (std::to_chars shortest round-trip reals).  Writes up to
+ * buflen bytes (NUL-terminated; buf may be NULL) and returns the full text
+ * length, or RPG_E_CSV ("cannot format an empty sample set", "metric 'x'
+ * has a non-finite value"). */
+int64_t rpg_samples_format(const int64_t* data, const int64_t* configs, const double* values,
+                           int64_t n, int32_t d, const char* const* metric_names,
+                           int32_t n_metrics, int32_t provenance_kind, uint64_t seed,
+                           double noise_rel, int32_t n_threads, char* buf, size_t buflen,
+                           char* err, size_t errlen);
 
 /* Specialized-kernel module statistics of this process: NVRTC compilations
  * and modules loaded from the persistent cubin cache (directory

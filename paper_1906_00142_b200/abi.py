@@ -34,6 +34,7 @@ RPG_E_NO_FEASIBLE = -5
 RPG_E_PIPELINE = -6
 RPG_E_FIT = -7
 RPG_E_EVAL = -8
+RPG_E_CSV = -9
 
 
 class rpg_profile(C.Structure):
@@ -69,6 +70,15 @@ class rpg_fit_trace(C.Structure):
     _fields_ = [("n_stages", C.c_int32), ("stop_reason", C.c_int32),
                 ("stage_coef", (C.c_double * RPG_FIT_MAX_COLS) * RPG_FIT_TRACE_STAGES),
                 ("round_qmin", C.c_double * RPG_FIT_TRACE_STAGES)]
+
+
+class rpg_fit_job(C.Structure):
+    _fields_ = [("y", C.POINTER(C.c_double)), ("num_bounds", C.POINTER(C.c_int32)),
+                ("den_bounds", C.POINTER(C.c_int32)), ("coef_out", C.POINTER(C.c_double)),
+                ("sigma_out", C.POINTER(C.c_double)), ("rank_out", C.POINTER(C.c_int32)),
+                ("truncated_out", C.POINTER(C.c_int32)), ("residual_out", C.POINTER(C.c_double)),
+                ("safeguard_out", C.POINTER(C.c_int32)), ("trace", C.POINTER(rpg_fit_trace)),
+                ("status", C.c_int32), ("message", C.c_char * 252)]
 
 
 # perf::MwpCwpBreakdown (perfmodel.hpp:284-296) + call status (rpg.h).
@@ -240,6 +250,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                               C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                               C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                               C.POINTER(rpg_fit_trace)) + errbuf),
+        "rpg_fit_rational_multi": (C.c_int, (C.POINTER(C.c_double), C.c_int64, C.c_int32,
+                                             C.POINTER(rpg_fit_job), C.c_int32, C.c_double,
+                                             C.c_int32) + errbuf),
         "rpg_program_plan_create": (C.c_int, (C.c_void_p, C.POINTER(rpg_profile),
                                               C.POINTER(rpg_config), C.c_int64,
                                               C.POINTER(rpg_options), C.c_int32,
@@ -283,6 +296,17 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "rpg_plan_group_size": (C.c_int32, (C.c_void_p,)),
         "rpg_search_batch_group": (C.c_int, (C.c_void_p, C.POINTER(C.c_int64), C.c_int64,
                                              C.c_int32, C.c_void_p) + errbuf),
+        "rpg_samples_parse": (C.c_int, (C.c_char_p, C.c_size_t, C.c_int32,
+                                        C.POINTER(C.c_void_p)) + errbuf),
+        "rpg_samples_info": (C.c_int, (C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_double))),
+        "rpg_samples_metric_name": (C.c_char_p, (C.c_void_p, C.c_int32)),
+        "rpg_samples_copy": (C.c_int, (C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)),
+        "rpg_samples_free": (None, (C.c_void_p,)),
+        "rpg_samples_format": (C.c_int64, (C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                           C.POINTER(C.c_char_p), C.c_int32, C.c_int32, C.c_uint64,
+                                           C.c_double, C.c_int32, C.c_char_p, C.c_size_t) + errbuf),
         "rpg_jit_stats": (None, (C.POINTER(C.c_int64), C.POINTER(C.c_int64))),
         "rpg_search": (C.c_int, (C.POINTER(rpg_model), C.POINTER(rpg_profile),
                                  C.POINTER(rpg_config), C.c_int64,
@@ -308,7 +332,9 @@ EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_aa_pack_degs", "rpg_aa_unpack_degs", "rpg_aa_from_poly",
                     "rpg_aa_to_poly", "rpg_emit_altarr_header", "rpg_jit_stats",
                     "rpg_plan_group_create", "rpg_plan_group_destroy", "rpg_plan_group_size",
-                    "rpg_search_batch_group", "rpg_fit_rational_traced",
+                    "rpg_search_batch_group", "rpg_fit_rational_traced", "rpg_fit_rational_multi",
+                    "rpg_samples_parse", "rpg_samples_info", "rpg_samples_metric_name",
+                    "rpg_samples_copy", "rpg_samples_free", "rpg_samples_format",
                     "rpg_mwpcwp_breakdown_batch")
 
 

@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "rpg.h"
@@ -1781,18 +1782,20 @@ extern "C" int rpg_fit_rational(const double* X, const double* y, int64_t m, int
                                  safeguard_out, nullptr, err, errlen);
 }
 
-extern "C" int rpg_fit_rational_traced(const double* X, const double* y, int64_t m, int32_t n_vars,
-                                       const int32_t* num_bounds, const int32_t* den_bounds,
-                                       double rank_tol, int32_t device, double* coef_out,
-                                       double* sigma_out, int32_t* rank_out,
-                                       int32_t* truncated_out, double* residual_out,
-                                       int32_t* safeguard_out, rpg_fit_trace* trace, char* err,
-                                       size_t errlen) {
+namespace {
+// One fit.  X: host samples (uploaded on this fit's stream), or dX: the
+// same samples already resident on `device` (rpg_fit_rational_multi shares
+// one upload between concurrent fits).
+int fit_impl(const double* X, const double* dXs, const double* y, int64_t m, int32_t n_vars,
+             const int32_t* num_bounds, const int32_t* den_bounds, double rank_tol,
+             int32_t device, double* coef_out, double* sigma_out, int32_t* rank_out,
+             int32_t* truncated_out, double* residual_out, int32_t* safeguard_out,
+             rpg_fit_trace* trace, char* err, size_t errlen) {
   if (trace) {
     *trace = rpg_fit_trace{};
     trace->stop_reason = RPG_FIT_STOP_NO_SAFEGUARD;
   }
-  if (m <= 0 || !X || !y) return fset_err(err, errlen, RPG_E_INVALID, "fit_rational: no samples");
+  if (m <= 0 || !(X || dXs) || !y) return fset_err(err, errlen, RPG_E_INVALID, "fit_rational: no samples");
   if (n_vars < 1 || n_vars > RPG_MAX_VARS || !num_bounds || !den_bounds)
     return fset_err(err, errlen, RPG_E_INVALID, "fit_rational: bad variable count");
   for (int v = 0; v < n_vars; ++v)
@@ -1836,10 +1839,12 @@ extern "C" int rpg_fit_rational_traced(const double* X, const double* y, int64_t
   int sms = 148;
   FCUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   DevBuf dX, dy, dexps, dR, dsig, dV, dscale, dc, dpart, dflags, dstats, dU;
-  FCUDA(fit_malloc((void**)&dX.p, sizeof(double) * (size_t)m * n_vars));
+  if (!dXs) {
+    FCUDA(fit_malloc((void**)&dX.p, sizeof(double) * (size_t)m * n_vars));
+    FCUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * (size_t)m * n_vars, cudaMemcpyHostToDevice, s));
+  }
   FCUDA(fit_malloc((void**)&dy.p, sizeof(double) * (size_t)m));
   FCUDA(fit_malloc((void**)&dexps.p, exps.size()));
-  FCUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * (size_t)m * n_vars, cudaMemcpyHostToDevice, s));
   FCUDA(cudaMemcpyAsync(dy.p, y, sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, s));
   FCUDA(cudaMemcpyAsync(dexps.p, exps.data(), exps.size(), cudaMemcpyHostToDevice, s));
   FCUDA(fit_malloc((void**)&dflags.p, sizeof(int) * 8));
@@ -1850,7 +1855,7 @@ extern "C" int rpg_fit_rational_traced(const double* X, const double* y, int64_t
   F.nn = nn;
   F.nd = nd;
   F.n = n;
-  F.X = dX.as<double>();
+  F.X = dXs ? dXs : dX.as<double>();
   F.y = dy.as<double>();
   F.w = nullptr;
   F.exps = dexps.as<uint8_t>();
@@ -1923,5 +1928,65 @@ extern "C" int rpg_fit_rational_traced(const double* X, const double* y, int64_t
   if (truncated_out) *truncated_out = flags[2] < n - 1;
   if (residual_out) *residual_out = nsig >= n ? sig[n - 1] : 0.0;
   if (safeguard_out) *safeguard_out = trigger;
+  return RPG_OK;
+}
+
+}  // namespace
+
+extern "C" int rpg_fit_rational_traced(const double* X, const double* y, int64_t m, int32_t n_vars,
+                                       const int32_t* num_bounds, const int32_t* den_bounds,
+                                       double rank_tol, int32_t device, double* coef_out,
+                                       double* sigma_out, int32_t* rank_out,
+                                       int32_t* truncated_out, double* residual_out,
+                                       int32_t* safeguard_out, rpg_fit_trace* trace, char* err,
+                                       size_t errlen) {
+  return fit_impl(X, nullptr, y, m, n_vars, num_bounds, den_bounds, rank_tol, device, coef_out,
+                  sigma_out, rank_out, truncated_out, residual_out, safeguard_out, trace, err,
+                  errlen);
+}
+
+// Several fits over one sample set (pipe::fit_all_metrics' loop, pipeline.hpp:
+// 145-184): X is uploaded once, then every job runs on its own host thread and
+// CUDA stream, so one fit's serial phases (the minimizer's per-step tail,
+// host polls) overlap the others' sample passes.  Each job's outcome is what
+// rpg_fit_rational returns for it alone (the fits are deterministic and
+// independent).
+extern "C" int rpg_fit_rational_multi(const double* X, int64_t m, int32_t n_vars,
+                                      rpg_fit_job* jobs, int32_t n_jobs, double rank_tol,
+                                      int32_t device, char* err, size_t errlen) {
+  if (m <= 0 || !X) return fset_err(err, errlen, RPG_E_INVALID, "fit_rational: no samples");
+  if (n_vars < 1 || n_vars > RPG_MAX_VARS)
+    return fset_err(err, errlen, RPG_E_INVALID, "fit_rational: bad variable count");
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs))
+    return fset_err(err, errlen, RPG_E_INVALID, "rpg_fit_rational_multi: bad job list");
+  if (n_jobs == 0) return RPG_OK;
+  FCUDA(cudaSetDevice(device));
+  cudaStream_t s;
+  FCUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  double* dX = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&dX, sizeof(double) * (size_t)m * n_vars, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(dX, X, sizeof(double) * (size_t)m * n_vars, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    if (dX) cudaFreeAsync(dX, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return fset_err(err, errlen, RPG_E_CUDA, "rpg_fit_rational_multi: %s", cudaGetErrorString(e));
+  }
+  std::vector<std::thread> th;
+  for (int32_t k = 0; k < n_jobs; ++k)
+    th.emplace_back([&, k] {
+      rpg_fit_job& J = jobs[k];
+      J.message[0] = 0;
+      cudaSetDevice(device);
+      J.status = fit_impl(nullptr, dX, J.y, m, n_vars, J.num_bounds, J.den_bounds, rank_tol,
+                          device, J.coef_out, J.sigma_out, J.rank_out, J.truncated_out,
+                          J.residual_out, J.safeguard_out, J.trace, J.message, sizeof J.message);
+    });
+  for (auto& t : th) t.join();
+  cudaFreeAsync(dX, s);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
   return RPG_OK;
 }

@@ -97,6 +97,79 @@ def fit_rational(X, y, variables: Sequence[str], num_bounds: Sequence[int],
     return f, rep
 
 
+def fit_rational_multi(X, ys: Sequence, variables: Sequence[str], bounds: Sequence[Tuple[Sequence[int], Sequence[int]]],
+                       rank_tol: float = K_DEFAULT_RANK_TOL, device: int = 0,
+                       traces: Optional[List[dict]] = None) -> List[object]:
+    """Several fit_rational calls over one sample matrix X, run concurrently
+    on the GPU (rpg_fit_rational_multi: X uploaded once, one stream per fit).
+    Returns per fit (RationalFunction, FitReport), or the DegenerateFit /
+    SvdFailure exception instance for a numerical failure."""
+    lib = A.load_library()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    if X.ndim == 1:
+        X = X[:, None]
+    m, nv = X.shape
+    k = len(ys)
+    jobs = (A.rpg_fit_job * max(k, 1))()
+    keep = []
+    shapes = []
+    for i, (y, (nb_, db_)) in enumerate(zip(ys, bounds)):
+        y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
+        if len(y) != m:
+            raise F.ModelError("fit_rational: points/values size mismatch")
+        nb, db = F.monomial_basis(nb_), F.monomial_basis(db_)
+        n = len(nb) + len(db)
+        arrs = dict(y=y, nbnd=np.ascontiguousarray(nb_, dtype=np.int32),
+                    dbnd=np.ascontiguousarray(db_, dtype=np.int32), coef=np.zeros(n),
+                    sig=np.zeros(max(1, min(m, n))), rank=np.zeros(1, np.int32),
+                    trunc=np.zeros(1, np.int32), resid=np.zeros(1), safe=np.zeros(1, np.int32),
+                    tr=A.rpg_fit_trace() if traces is not None else None)
+        keep.append(arrs)
+        shapes.append((nb, db, n))
+        J = jobs[i]
+        J.y = A.ptr(arrs["y"], C.c_double)
+        J.num_bounds = A.ptr(arrs["nbnd"], C.c_int32)
+        J.den_bounds = A.ptr(arrs["dbnd"], C.c_int32)
+        J.coef_out = A.ptr(arrs["coef"], C.c_double)
+        J.sigma_out = A.ptr(arrs["sig"], C.c_double)
+        J.rank_out = A.ptr(arrs["rank"], C.c_int32)
+        J.truncated_out = A.ptr(arrs["trunc"], C.c_int32)
+        J.residual_out = A.ptr(arrs["resid"], C.c_double)
+        J.safeguard_out = A.ptr(arrs["safe"], C.c_int32)
+        if arrs["tr"] is not None:
+            J.trace = C.pointer(arrs["tr"])
+    err = C.create_string_buffer(512)
+    rc = lib.rpg_fit_rational_multi(A.ptr(X, C.c_double), m, nv, jobs, k, rank_tol, device, err, len(err))
+    if rc != A.RPG_OK:
+        msg = err.value.decode()
+        raise ValueError(msg) if rc == A.RPG_E_INVALID else A.RpgError(rc, msg)
+    out: List[object] = []
+    for i in range(k):
+        J, arrs, (nb, db, n) = jobs[i], keep[i], shapes[i]
+        if traces is not None:
+            tr = arrs["tr"]
+            started = tr.n_stages - 1 + (1 if tr.stop_reason in (1, 2) else 0) if tr.n_stages >= 2 else 0
+            traces.append({"stages": [np.array(tr.stage_coef[s_][:n]) for s_ in range(tr.n_stages)],
+                           "round_qmin": [float(tr.round_qmin[s_]) for s_ in range(started)],
+                           "stop": A.FIT_STOP_NAMES.get(tr.stop_reason, str(tr.stop_reason))})
+        if J.status != A.RPG_OK:
+            msg = J.message.decode(errors="replace")
+            if J.status == A.RPG_E_INVALID:
+                raise ValueError(msg)
+            if J.status == A.RPG_E_FIT:
+                out.append((SvdFailure if msg.startswith("svd") else DegenerateFit)(msg))
+                continue
+            raise A.RpgError(J.status, msg)
+        coef = arrs["coef"]
+        f = F.RationalFunction(F.Polynomial(list(variables), nb, list(coef[: len(nb)])),
+                               F.Polynomial(list(variables), db, list(coef[len(nb):])))
+        rep = FitReport(residual_norm=float(arrs["resid"][0]), numerical_rank=int(arrs["rank"][0]),
+                        singular_values=list(arrs["sig"][: min(m, n)]), truncated=bool(arrs["trunc"][0]),
+                        safeguard=bool(arrs["safe"][0]))
+        out.append((f, rep))
+    return out
+
+
 def default_bounds(n_variables: int) -> Tuple[List[int], List[int]]:
     """pipe::default_bounds (pipeline.hpp:88-93)."""
     return [2] * n_variables, [1] * n_variables
@@ -133,8 +206,22 @@ def fit_metrics(X, metric_values: Dict[str, np.ndarray], variables: Sequence[str
     """Fits the listed metrics; per metric the outcome is (RationalFunction,
     report dict) or, for a numerical failure (``fit_fn`` raised DegenerateFit
     or SvdFailure), the failure message (str)."""
-    fit_fn = fit_fn or (lambda X_, y_, v_, nb_, db_, tol_: fit_rational(X_, y_, v_, nb_, db_, tol_, device))
     out: Dict[str, object] = {}
+    if fit_fn is None:
+        # the GPU fit: every metric at once (one upload of X, concurrent fits)
+        res = fit_rational_multi(X, [metric_values[mt] for mt in metrics], variables,
+                                 [bounds.get(mt, default_bounds(len(variables))) for mt in metrics],
+                                 rank_tol, device)
+        for metric, r in zip(metrics, res):
+            if isinstance(r, Exception):
+                out[metric] = str(r)
+            else:
+                f, rep = r
+                out[metric] = (f, {"residual_norm": rep.residual_norm,
+                                   "numerical_rank": rep.numerical_rank,
+                                   "truncated": rep.truncated,
+                                   "singular_values": list(rep.singular_values)})
+        return out
     for metric in metrics:
         nb, db = bounds.get(metric, default_bounds(len(variables)))
         try:

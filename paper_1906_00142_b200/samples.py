@@ -96,146 +96,59 @@ def cpp_to_string(v: float) -> str:
 
 
 # ---------------------------------------------------------------------------
-# CSV (datakit.hpp:272-415)
+# CSV (datakit.hpp:272-415): native, columnar, multi-threaded (rpg_csv.cpp
+# behind rpg_samples_parse / rpg_samples_format).
 
-def _split_csv(line: str) -> List[str]:
-    return ["".join(ch for ch in f if ch not in "\r \t") for f in line.split(",")]
-
-
-def _parse_int(s: str, line_no: int, what: str) -> int:
-    # std::from_chars(long long): optional '-', decimal digits, nothing else
-    body = s[1:] if s.startswith("-") else s
-    if not body or not body.isascii() or not body.isdigit():
-        raise CsvError(f"line {line_no}: bad integer {what} '{s}'")
-    v = int(s)
-    if not -(1 << 63) <= v < (1 << 63):
-        raise CsvError(f"line {line_no}: bad integer {what} '{s}'")
-    return v
-
-
-def _parse_real(s: str, line_no: int, what: str) -> float:
-    # std::from_chars(double), general format: no leading '+', no
-    # whitespace, no hex prefix; inf/nan spellings parse but are rejected as
-    # non-finite.
-    ok = bool(s) and s[0] != "+" and s.isascii() and "_" not in s and not s.lower().startswith(("0x", "-0x"))
+def parse_samples(text, n_threads: int = 0) -> SampleSet:
+    """data::parse_samples (datakit.hpp:329-412) — same schema, checks,
+    error precedence and CsvError messages — parsed by librpgpu (columnar,
+    all host threads by default).  ``text``: str or bytes."""
+    lib = A.load_library()
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    rc = lib.rpg_samples_parse(raw, len(raw), n_threads, C.byref(h), err, len(err))
+    if rc == A.RPG_E_CSV:
+        raise CsvError(err.value.decode(errors="replace"))
+    A.check(rc, err)
     try:
-        v = float(s) if ok else None
-    except ValueError:
-        v = None
-    if v is None:
-        raise CsvError(f"line {line_no}: bad value for {what} '{s}'")
-    if not math.isfinite(v):
-        raise CsvError(f"line {line_no}: non-finite value for {what}")
-    return v
+        n, d, k, kind = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32()
+        seed, noise = C.c_uint64(), C.c_double()
+        lib.rpg_samples_info(h, C.byref(n), C.byref(d), C.byref(k), C.byref(kind), C.byref(seed),
+                             C.byref(noise))
+        names = [lib.rpg_samples_metric_name(h, i).decode() for i in range(k.value)]
+        data = np.zeros((n.value, d.value), dtype=np.int64)
+        cfg = np.zeros((n.value, 3), dtype=np.int64)
+        vals = np.zeros((n.value, k.value), dtype=np.float64)
+        lib.rpg_samples_copy(h, data.ctypes.data_as(C.c_void_p), cfg.ctypes.data_as(C.c_void_p),
+                             vals.ctypes.data_as(C.c_void_p))
+    finally:
+        lib.rpg_samples_free(h)
+    prov = Provenance("synthetic", seed.value, noise.value) if kind.value == 1 else Provenance()
+    return SampleSet(names, data, cfg, vals, prov)
 
 
-def parse_samples(text: str) -> SampleSet:
-    """data::parse_samples (datakit.hpp:329-412)."""
-    prov = Provenance()
-    names: List[str] = []
-    d = 0
-    have_header = False
-    rows_d, rows_c, rows_v = [], [], []
-    seen = set()
-    for line_no, line in enumerate(text.split("\n"), start=1):
-        if line.endswith("\r"):
-            line = line[:-1]
-        if line.strip(" \t") == "":
-            continue
-        if line[0] == "#":
-            if have_header:
-                raise CsvError(f"line {line_no}: comments are only allowed before the header")
-            toks = line.split()
-            tag = toks[1] if len(toks) > 1 else ""
-            kind = toks[2] if len(toks) > 2 else ""
-            if tag == "provenance:":
-                if kind == "measured":
-                    prov = Provenance()
-                elif kind == "synthetic":
-                    prov.kind = "synthetic"
-                    for kv in toks[3:]:
-                        if "=" not in kv:
-                            continue
-                        key, val = kv.split("=", 1)
-                        if key == "seed":
-                            try:
-                                if not val.strip().lstrip("+").isdigit():
-                                    raise ValueError
-                                prov.seed = int(val) % (1 << 64)
-                            except ValueError:
-                                raise CsvError(f"line {line_no}: bad provenance seed '{val}'") from None
-                        elif key == "noise_rel":
-                            prov.noise_rel = _parse_real(val, line_no, "noise_rel")
-                else:
-                    raise CsvError(f"line {line_no}: unknown provenance kind '{kind}'")
-            continue
-        fields = _split_csv(line)
-        if not have_header:
-            i = 0
-            while i < len(fields) and fields[i] == f"D{i + 1}":
-                i += 1
-            d = i
-            if d == 0:
-                raise CsvError(f"line {line_no}: header must start with data-parameter columns "
-                               "D1,...,Dd")
-            if len(fields) < d + 4:
-                raise CsvError(f"line {line_no}: header is missing block-dimension or metric "
-                               "columns")
-            if fields[d] != "bx" or fields[d + 1] != "by" or fields[d + 2] != "bz":
-                raise CsvError(f"line {line_no}: header must list bx,by,bz after the data "
-                               "parameters")
-            for k in range(d + 3, len(fields)):
-                if not fields[k]:
-                    raise CsvError(f"line {line_no}: empty metric column name")
-                if fields[k] in names:
-                    raise CsvError(f"line {line_no}: duplicate metric column '{fields[k]}'")
-                names.append(fields[k])
-            have_header = True
-            continue
-        want = d + 3 + len(names)
-        if len(fields) != want:
-            raise CsvError(f"line {line_no}: expected {want} fields, found {len(fields)}")
-        dp = tuple(_parse_int(fields[i], line_no, f"D{i + 1}") for i in range(d))
-        cfg = (_parse_int(fields[d], line_no, "bx"), _parse_int(fields[d + 1], line_no, "by"),
-               _parse_int(fields[d + 2], line_no, "bz"))
-        if min(cfg) < 1:
-            raise CsvError(f"line {line_no}: block dimensions must be positive")
-        vals = [_parse_real(fields[d + 3 + k], line_no, names[k]) for k in range(len(names))]
-        if (dp, cfg) in seen:
-            raise CsvError(f"line {line_no}: duplicate sample for the same point and configuration")
-        seen.add((dp, cfg))
-        rows_d.append(dp)
-        rows_c.append(cfg)
-        rows_v.append(vals)
-    if not have_header:
-        raise CsvError("no header row found")
-    n = len(rows_c)
-    return SampleSet(names, np.array(rows_d, dtype=np.int64).reshape(n, d),
-                     np.array(rows_c, dtype=np.int64).reshape(n, 3),
-                     np.array(rows_v, dtype=np.float64).reshape(n, len(names)), prov)
-
-
-def format_samples(s: SampleSet) -> str:
-    """data::format_samples (datakit.hpp:286-326)."""
-    if len(s) == 0:
-        raise CsvError("cannot format an empty sample set")
-    out = []
-    if s.provenance.kind == "synthetic":
-        out.append(f"# provenance: synthetic seed={s.provenance.seed} "
-                   f"noise_rel={format_double(s.provenance.noise_rel)}")
-    else:
-        out.append("# provenance: measured")
-    d = s.dims()
-    out.append("".join(f"D{i}," for i in range(1, d + 1)) + "bx,by,bz" +
-               "".join("," + m for m in s.metric_names))
-    if not np.isfinite(s.values).all():
-        bad = int(np.argwhere(~np.isfinite(s.values))[0][1])
-        raise CsvError(f"metric '{s.metric_names[bad]}' has a non-finite value")
-    for i in range(len(s)):
-        out.append("".join(f"{int(p)}," for p in s.data[i]) +
-                   f"{int(s.configs[i, 0])},{int(s.configs[i, 1])},{int(s.configs[i, 2])}" +
-                   "".join("," + format_double(v) for v in s.values[i]))
-    return "\n".join(out) + "\n"
+def format_samples(s: SampleSet, n_threads: int = 0) -> str:
+    """data::format_samples (datakit.hpp:286-326), formatted by librpgpu
+    (std::to_chars shortest round-trip reals)."""
+    lib = A.load_library()
+    n = len(s)
+    d = s.dims() if n else int(s.data.shape[1]) if s.data.ndim == 2 else 0
+    data = np.ascontiguousarray(s.data, dtype=np.int64).reshape(n, d)
+    cfg = np.ascontiguousarray(s.configs, dtype=np.int64).reshape(n, 3)
+    vals = np.ascontiguousarray(s.values, dtype=np.float64).reshape(n, len(s.metric_names))
+    names = (C.c_char_p * max(1, len(s.metric_names)))(*[m.encode() for m in s.metric_names])
+    kind = 1 if s.provenance.kind == "synthetic" else 0
+    err = C.create_string_buffer(512)
+    args = (data.ctypes.data_as(C.c_void_p), cfg.ctypes.data_as(C.c_void_p),
+            vals.ctypes.data_as(C.c_void_p), n, d, names, len(s.metric_names), kind,
+            int(s.provenance.seed) % (1 << 64), float(s.provenance.noise_rel), 0)
+    need = lib.rpg_samples_format(*args, None, 0, err, len(err))
+    if need < 0:
+        raise CsvError(err.value.decode(errors="replace"))
+    buf = C.create_string_buffer(need + 1)
+    lib.rpg_samples_format(*args, buf, need + 1, err, len(err))
+    return buf.raw[:need].decode()
 
 
 def read_samples(path: str) -> SampleSet:

@@ -152,3 +152,30 @@ def test_large_sample_matches_o3():
     assert rep.numerical_rank == ro.numerical_rank and rep.safeguard == ro.safeguard
     Xh = X[:2000]
     assert np.max(np.abs(ev(f, Xh) - ev(fo, Xh)) / np.abs(ev(fo, Xh))) < 1e-6
+
+
+def test_multi_fit_equals_one_by_one():
+    """rpg_fit_rational_multi (X uploaded once, the fits concurrent on their
+    own streams) returns exactly what one rpg_fit_rational call per metric
+    returns — coefficients, singular values, rank, safeguard — including a
+    failing job, which fails alone."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    X, ys, var = bench.c4_data(200_000, 0.01)
+    names = sorted(ys)
+    ys_list = [ys[k] for k in names] + [np.zeros(len(X))]
+    bnds = [([2, 2, 2], [1, 1, 1])] * len(names) + [([1, 1, 1], [0, 0, 0])]
+    got = G.fit_rational_multi(X, ys_list, var, bnds)
+    assert len(got) == len(ys_list)
+    for y, (nb, db), g in zip(ys_list, bnds, got):
+        try:
+            f, rep = G.fit_rational(X, y, var, nb, db)
+        except (G.DegenerateFit, G.SvdFailure) as e:
+            assert isinstance(g, type(e)) and str(g) == str(e)
+            continue
+        gf, grep = g
+        assert gf.num.coeffs == f.num.coeffs and gf.den.coeffs == f.den.coeffs
+        assert grep.singular_values == rep.singular_values
+        assert (grep.numerical_rank, grep.safeguard, grep.truncated) == (rep.numerical_rank, rep.safeguard, rep.truncated)

@@ -62,12 +62,23 @@ def main():
                 safeguards[name] = f"failed: {e}"
         times.append(time.perf_counter() - t0)
     gpu_s = min(times)
+    # the fit_all_metrics path: every metric at once (rpg_fit_rational_multi)
+    times_multi = []
+    names = list(ys)
+    for _ in range(args.reps):
+        t0 = time.perf_counter()
+        res = G.fit_rational_multi(X, [ys[k] for k in names], spec.variables, [(nb, db)] * len(names))
+        times_multi.append(time.perf_counter() - t0)
+    multi = {k: (r[1].safeguard if not isinstance(r, Exception) else f"failed: {r}") for k, r in zip(names, res)}
     n = 35
     flops = len(ys) * (2 * m * n * n - 2 * n ** 3 / 3 + 3 * m * n)  # BASELINE.md C4 formula
     line = {"metric": "C4 rational fit time (5 metrics)", "samples_per_metric": m, "columns": n,
             "noise_rel": args.noise, "gpu_seconds": gpu_s, "gpu_samples_per_s": len(ys) * m / gpu_s,
             "qr_flops": flops, "gpu_tflops_qr_equiv": flops / gpu_s / 1e12,
-            "safeguard": safeguards, "api": "rpg_fit_rational (host buffers, incl. H2D)"}
+            "safeguard": safeguards, "api": "rpg_fit_rational (host buffers, incl. H2D), one metric after another",
+            "multi_seconds": min(times_multi), "multi_samples_per_s": len(ys) * m / min(times_multi),
+            "multi_outcomes_equal": multi == safeguards,
+            "multi_api": "rpg_fit_rational_multi (X uploaded once, 5 concurrent fits)"}
     if args.cpu:
         t0 = time.perf_counter()
         for name, y in ys.items():
