@@ -143,12 +143,17 @@ def format_samples(s: SampleSet, n_threads: int = 0) -> str:
     args = (data.ctypes.data_as(C.c_void_p), cfg.ctypes.data_as(C.c_void_p),
             vals.ctypes.data_as(C.c_void_p), n, d, names, len(s.metric_names), kind,
             int(s.provenance.seed) % (1 << 64), float(s.provenance.noise_rel), 0)
-    need = lib.rpg_samples_format(*args, None, 0, err, len(err))
+    # one pass into a buffer sized for the longest possible rows (int64: 20
+    # chars + sign; shortest-round-trip double: at most 24 chars)
+    cap = 256 + sum(len(m) + 1 for m in s.metric_names) + n * (22 * (d + 3) + 25 * len(s.metric_names) + 1)
+    buf = C.create_string_buffer(cap)
+    need = lib.rpg_samples_format(*args, buf, cap, err, len(err))
     if need < 0:
         raise CsvError(err.value.decode(errors="replace"))
-    buf = C.create_string_buffer(need + 1)
-    lib.rpg_samples_format(*args, buf, need + 1, err, len(err))
-    return buf.raw[:need].decode()
+    if need >= cap:  # cannot happen with the bound above; stay correct anyway
+        buf = C.create_string_buffer(need + 1)
+        need = lib.rpg_samples_format(*args, buf, need + 1, err, len(err))
+    return C.string_at(buf, need).decode("ascii")
 
 
 def read_samples(path: str) -> SampleSet:
