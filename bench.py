@@ -67,7 +67,16 @@ class Workload:
         from paper_1906_00142_b200 import formats as F
         self.name = name
         self.hw = F.load_profile(os.path.join(ROOT, "data", "b200.profile"))
-        if name == "c5":
+        if name == "c6":
+            self.kernels = ("c6_stencil", "c6_kloop", "c6_reduce")
+            path = os.path.join(ROOT, "data", "stressed", "{}.models.json")
+            self.space = F.integer_configs(1024, dims=2)
+            self.scaling = "strong"
+            self.describe = ("C6 non-degenerate landscape (data/stressed/make_c6.py): 3 T-symmetric synthetic "
+                             "kernels (default-bound fitted form), regs 80 (22.5% of points infeasible), "
+                             "exact multi-member tie groups, all three MWP-CWP cases; N = 64..65536 x 7262 "
+                             "integer (bx,by), B200 profile")
+        elif name == "c5":
             self.kernels = ("stencil3d_nm",)
             path = os.path.join(ROOT, "data", "stress", "{}.models.json")
             self.space = F.integer_configs(1024, dims=3)
@@ -128,9 +137,9 @@ def official_flops(spec) -> int:
 
 def default_arith(workload: str, kernel: str) -> str:
     """The arithmetic mode a workload is benchmarked in: the configuration-
-    major FAST_CM search for the one-data-parameter C2/C3 models (specialized
+    major FAST_CM search for the one-data-parameter C2/C3/C6 models (specialized
     kernels only), FAST otherwise (C5's two data parameters, the Ec dump)."""
-    return "fastcm" if workload in ("c2", "c3") and kernel == "specialized" else "fast"
+    return "fastcm" if workload in ("c2", "c3", "c6") and kernel == "specialized" else "fast"
 
 
 def count_kernel_launches(fn, prefix="rpg_"):
@@ -722,7 +731,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5", "dump"], default="c2",
+    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5", "c6", "dump"], default="c2",
                     help="BASELINE.json config: c2 (default, configs[1]), c3 (full suite), c5 (stress)")
     ap.add_argument("--arith", choices=["exact", "fast", "fastcm"], default=None,
                     help="default: fastcm (configuration-major) for the one-data-parameter C2/C3 "

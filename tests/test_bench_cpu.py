@@ -21,7 +21,7 @@ def test_c2_is_configs1():
     assert len(t) == 65473 and t[0, 0] == 64 and t[-1, 0] == 65536 and np.all(np.diff(t[:, 0]) == 1)
 
 
-@pytest.mark.parametrize("name,count", [("c2", 65473), ("c3", 65473), ("c5", 182 * 182)])
+@pytest.mark.parametrize("name,count", [("c2", 65473), ("c3", 65473), ("c5", 182 * 182), ("c6", 65473)])
 def test_strong_partitions_cover_every_tuple_once(name, count):
     w = bench.Workload(name)
     assert w.scaling == "strong"
@@ -80,3 +80,11 @@ def test_default_arith_per_workload():
     assert bench.default_arith("c5", "specialized") == "fast"
     assert bench.default_arith("dump", "specialized") == "fast"
     assert bench.default_arith("c2", "generic") == "fast"
+
+
+def test_c6_is_the_non_degenerate_landscape():
+    w = bench.Workload("c6")
+    assert w.kernels == ("c6_stencil", "c6_kloop", "c6_reduce") and len(w.space) == 7262
+    assert bench.default_arith("c6", "specialized") == "fastcm"
+    for spec in w.specs.values():
+        assert spec.constants["regs_per_thread"] == 80.0
