@@ -967,6 +967,197 @@ min_prep(const double* __restrict__ R, const double* __restrict__ S, int nn, int
 // KKT [H g; g^T 0] [dc; l] = [-grad; 0] solved by Gaussian elimination with
 // partial pivoting (the reference uses LDLT), decrement = -grad.dc,
 // phi0 = ||A_eq c||^2 - mu sum log q.  One CTA.
+// ---------------------------------------------------------------------------
+// Warp-parallel pieces of the minimizer's serial tail (one CTA of
+// kFitThreads threads; R and the Schur factors staged in SMEM).
+
+__device__ __forceinline__ double warp_sum(double t) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+// rows[i] = (R S (c + alpha dc))[i] = sum_{k >= i} R[i][k] S[k] (c[k] + alpha
+// dc[k]), one warp per row, lanes over k, a fixed shuffle tree — the same
+// bits for the Newton step's phi0 (alpha = 0, dc = null) and the line
+// search's candidates.
+__device__ __forceinline__ void rs_rows(const double* R, const double* __restrict__ S,
+                                        const double* __restrict__ c, const double* __restrict__ dc,
+                                        double alpha, int n, double* rows, int warp0, int nwarps) {
+  const int warp = (int)(threadIdx.x >> 5) - warp0, lane = threadIdx.x & 31;
+  if (warp < 0 || warp >= nwarps) return;
+  for (int i = warp; i < n; i += nwarps) {
+    double t = 0.0;
+    for (int k = i + lane; k < n; k += 32)
+      t = fma(R[i * n + k], S[k] * (dc ? c[k] + alpha * dc[k] : c[k]), t);
+    t = warp_sum(t);
+    if (lane == 0) rows[i] = t;
+  }
+}
+
+// sum_i rows[i]^2 over n <= 64 rows: one warp, lanes i and i + 32, then the
+// shuffle tree (fixed order).  Lane 0 returns it.
+__device__ __forceinline__ double sumsq_rows(const double* rows, int n) {
+  const int lane = threadIdx.x & 31;
+  double t = 0.0;
+  if (lane < n) t = rows[lane] * rows[lane];
+  if (lane + 32 < n) t = fma(rows[lane + 32], rows[lane + 32], t);
+  return warp_sum(t);
+}
+
+// Gaussian elimination with partial pivoting (first largest |pivot|) of the
+// Schur system [K | rhs] with M = nd + 1 <= 9 rows, one warp: lane r holds
+// row r in registers, padded with identity rows up to 9 (they never win a
+// pivot of a real column).  On return lane r < M holds x_r; *singular when
+// a pivot is zero.
+__device__ __forceinline__ double ge9_warp(double (&a)[10], int M, bool* singular) {
+  const int lane = threadIdx.x & 31;
+  bool sing = false;
+#pragma unroll
+  for (int col = 0; col < 9; ++col) {
+    double v = (lane >= col && lane < 9) ? fabs(a[col]) : -1.0;
+    int p = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int op = __shfl_xor_sync(0xffffffffu, p, o);
+      if (ov > v || (ov == v && op < p)) {
+        v = ov;
+        p = op;
+      }
+    }
+    if (col < M && v == 0.0) sing = true;
+    // swap rows col and p
+#pragma unroll
+    for (int j = 0; j < 10; ++j) {
+      const double from_p = __shfl_sync(0xffffffffu, a[j], p);
+      const double from_c = __shfl_sync(0xffffffffu, a[j], col);
+      if (lane == col) a[j] = from_p;
+      else if (lane == p) a[j] = from_c;
+    }
+    double prow[10];
+#pragma unroll
+    for (int j = 0; j < 10; ++j) prow[j] = __shfl_sync(0xffffffffu, a[j], col);
+    if (lane > col && lane < 9) {
+      const double f = a[col] / prow[col];
+#pragma unroll
+      for (int j = col + 1; j < 10; ++j) a[j] -= f * prow[j];
+    }
+  }
+  double x = 0.0;  // lane r: x_r after back substitution
+#pragma unroll
+  for (int r = 8; r >= 0; --r) {
+    // t = rhs_r - sum_{j > r} a[r][j] x_j, on lane r
+    double t = a[9];
+#pragma unroll
+    for (int j = r + 1; j < 9; ++j) t -= a[j] * __shfl_sync(0xffffffffu, x, j);
+    if (lane == r) x = t / a[r];
+  }
+  *singular = sing;
+  return x;
+}
+
+// The Schur-complement Newton step (see min_prep) for nd <= 8, all stages
+// warp-parallel: RSc = R S c, H0c = S R^T RSc, grad, t = A^-1 (-grad_u),
+// the (nd+1)-square KKT system in one warp's registers, dc, the decrement
+// and phi0 = ||R S c||^2 - mu sum log q.  P: the min_prep factors in SMEM.
+__device__ void newton_schur_fast(const double* R, const double* __restrict__ S,
+                                  const double* __restrict__ gsum,
+                                  const double* __restrict__ pass_out,
+                                  const double* __restrict__ c, int nn, int nd,
+                                  double* __restrict__ dc, const double mu,
+                                  MinState* __restrict__ st, const double* P, double* ws) {
+  const int n = nn + nd;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* RSc = ws;           // 64
+  double* grad = ws + 64;     // 64
+  double* tu = ws + 128;      // 64
+  double* rhs = ws + 192;     // 16
+  double* xs = ws + 208;      // 16
+  const double* gq = pass_out + 2 * kAlphas;
+  const double* G = gq + nd;
+  const double* Ainv = P + 1;
+  const double* B = Ainv + nn * nn;
+  const double* Fm = B + nn * nd;
+  const double* Sv0 = Fm + nn * nd;
+  rs_rows(R, S, c, nullptr, 0.0, n, RSc, 0, nw);
+  __syncthreads();
+  for (int k = warp; k < n; k += nw) {
+    double t = 0.0;
+    for (int i = lane; i <= k; i += 32) t = fma(R[i * n + k], RSc[i], t);
+    t = warp_sum(t);
+    if (lane == 0) grad[k] = 2.0 * (S[k] * t) - mu * (k >= nn ? S[k] * gq[k - nn] : 0.0);
+  }
+  __syncthreads();
+  for (int i = warp; i < nn; i += nw) {
+    double t = 0.0;
+    for (int k = lane; k < nn; k += 32) t = fma(Ainv[i * nn + k], -grad[k], t);
+    t = warp_sum(t);
+    if (lane == 0) tu[i] = t;
+  }
+  __syncthreads();
+  for (int a = warp; a < nd; a += nw) {
+    double t = 0.0;
+    for (int k = lane; k < nn; k += 32) t = fma(B[k * nd + a], tu[k], t);
+    t = warp_sum(t);
+    if (lane == 0) rhs[a] = -grad[nn + a] - t;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int M = nd + 1;
+    // columns 0..nd-1: dv, nd: the multiplier, nd+1..8: identity padding,
+    // 9: right-hand side
+    double row[10];
+#pragma unroll
+    for (int j = 0; j < 10; ++j) row[j] = 0.0;
+    if (lane < nd) {
+      const double sa = S[nn + lane];
+#pragma unroll
+      for (int b = 0; b < 9; ++b) {
+        if (b < nd) row[b] = Sv0[lane * nd + b] + mu * sa * S[nn + b] * G[lane * nd + b];
+        else if (b == nd) row[b] = gsum[lane] * sa;
+      }
+      row[9] = rhs[lane];
+    } else if (lane == nd) {
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (b < nd) row[b] = gsum[b] * S[nn + b];
+    } else if (lane < 9) {
+#pragma unroll
+      for (int b = 0; b < 9; ++b)
+        if (b == lane) row[b] = 1.0;
+    }
+    bool sing;
+    const double x = ge9_warp(row, M, &sing);
+    if (lane < nd) xs[lane] = x;
+    if (lane == 0) st->ok = sing ? 0 : 1;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+    double t = tu[i];
+    for (int j = 0; j < nd; ++j) t -= Fm[i * nd + j] * xs[j];
+    dc[i] = t;
+  }
+  for (int j = threadIdx.x; j < nd; j += blockDim.x) dc[nn + j] = xs[j];
+  __syncthreads();
+  if (warp == 0) {
+    double d = 0.0;
+    bool fin = true;
+    for (int k = lane; k < n; k += 32) {
+      fin &= isfinite(dc[k]);
+      d = fma(-grad[k], dc[k], d);
+    }
+    d = warp_sum(d);
+    fin = __all_sync(0xffffffffu, fin);
+    const double a2 = sumsq_rows(RSc, n);
+    if (lane == 0) {
+      st->ok = (st->ok && fin) ? 1 : 0;
+      st->decrement = d;
+      st->phi0 = a2 - mu * pass_out[1];
+    }
+  }
+}
+
 __device__ void newton_body(const double* __restrict__ R, const double* __restrict__ S,
                             const double* __restrict__ gsum, const double* __restrict__ pass_out,
                             const double* __restrict__ c, int nn, int nd, double* __restrict__ dc,
@@ -980,6 +1171,10 @@ __device__ void newton_body(const double* __restrict__ R, const double* __restri
   double* grad = RSc + n;          // n
   const double* gq = pass_out + 2 * kAlphas;
   const double* G = gq + nd;
+  if (prep && prep[kPrepOk] != 0.0 && nd <= 8 && n <= 64) {
+    newton_schur_fast(R, S, gsum, pass_out, c, nn, nd, dc, mu, st, prep, K);
+    return;
+  }
   // RSc = R S c
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double t = 0.0;
@@ -1214,10 +1409,14 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
   {
     extern __shared__ __align__(16) double fsm[];
     double* Rs = fsm + (n + 1) * (n + 2) + 3 * n;  // behind newton_body's workspace
+    double* Ps = Rs + n * n;                       // the min_prep factors
     __syncthreads();
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) Rs[e] = R[e];
+    if (prep && ph == kMinNewton)
+      for (int e = threadIdx.x; e < prep_size(nn, nd); e += blockDim.x) Ps[e] = prep[e];
     __syncthreads();
     R = Rs;
+    if (prep && ph == kMinNewton) prep = Ps;
   }
   if (ph == kMinNewton) {
     newton_body(R, S, gsum, pass_out, c, nn, nd, dc, ctl->mu, scratch, prep);
@@ -1245,22 +1444,19 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int na = ctl->n_alpha;
   __shared__ double rows[kAlphas][kMaxCols];
+  // ||R S cn||^2 per candidate: the rows as the Newton step's phi0 forms
+  // them (rs_rows: the same bits per row whichever warp computes it), two
+  // warps per candidate, then the fixed-order sum of squares.
+  {
+    const int nw = blockDim.x >> 5, per = nw / kAlphas > 0 ? nw / kAlphas : 1;
+    for (int a = 0; a < na; ++a)
+      if (warp / per == a || (per == 0 && warp == a))
+        rs_rows(R, S, c, dc, ctl->al[a], n, rows[a], a * per, per);
+  }
+  __syncthreads();
   if (warp < na) {
-    // ||R S cn||^2 with the row sums in parallel and the sum of squares in
-    // row order — the operation order of phi0 (newton_body), so a step of
-    // vanishing length reproduces phi0 exactly.
-    const double al = ctl->al[warp];
-    for (int i = lane; i < n; i += 32) {
-      double t = 0.0;
-      for (int k = i; k < n; ++k) t = fma(R[i * n + k], S[k] * (c[k] + al * dc[k]), t);
-      rows[warp][i] = t;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      double acc = 0.0;
-      for (int i = 0; i < n; ++i) acc = fma(rows[warp][i], rows[warp][i], acc);
-      phis[warp] = acc - ctl->mu * pass_out[2 * warp + 1];
-    }
+    const double acc = sumsq_rows(rows[warp], n);
+    if (lane == 0) phis[warp] = acc - ctl->mu * pass_out[2 * warp + 1];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1305,7 +1501,7 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
 constexpr int kStepGroup = 32;
 
 template <int NDT>
-__global__ void __launch_bounds__(kFitThreads)
+__global__ void __launch_bounds__(kFitThreads, NDT == 8 ? 4 : 2)
 min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __restrict__ pass_out,
          unsigned* __restrict__ counter /* n_groups + 1 */, double* __restrict__ gpart,
          const double* __restrict__ R, const double* __restrict__ S,
@@ -1603,7 +1799,8 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   FCUDA(cudaStreamSynchronize(s));
   if (!hs.ok) return RPG_OK;
   // newton_body's KKT workspace + the staged R (ctl_step_body)
-  const size_t smk = sizeof(double) * ((size_t)(n + 1) * (n + 2) + 3 * (size_t)n + (size_t)n * n);
+  const size_t smk = sizeof(double) * ((size_t)(n + 1) * (n + 2) + 3 * (size_t)n + (size_t)n * n +
+                                        (size_t)prep_size(nn, nd));
   DevBuf ctlb;
   FCUDA(fit_malloc((void**)&ctlb.p, sizeof(MinCtl)));
   MinCtl hc{};
