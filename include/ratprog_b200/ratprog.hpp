@@ -31,6 +31,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <charconv>
 #include <cmath>
 #include <cstdint>
@@ -63,29 +64,28 @@ struct DegreeBounds {
   std::vector<int> num, den;
 };
 
-// Graded-lex exponent tuples (polyfit.hpp:50-73).
+// Graded-lex exponent tuples (polyfit.hpp:50-73): every tuple e with
+// 0 <= e_i <= bounds_i, grouped by total degree (ascending), each group in
+// lexicographic order.  Built with a mixed-radix counter (lex order) whose
+// tuples are appended to their degree's bucket.
 inline std::vector<std::vector<int>> monomial_basis(const std::vector<int>& bounds) {
   for (int b : bounds)
     if (b < 0) throw std::invalid_argument("negative degree bound");
-  std::vector<std::vector<int>> tuples{{}};
-  for (int b : bounds) {
-    std::vector<std::vector<int>> next;
-    next.reserve(tuples.size() * (b + 1));
-    for (const auto& t : tuples)
-      for (int e = 0; e <= b; ++e) {
-        next.push_back(t);
-        next.back().push_back(e);
-      }
-    tuples = std::move(next);
+  const size_t nv = bounds.size();
+  const int max_deg = std::accumulate(bounds.begin(), bounds.end(), 0);
+  std::vector<std::vector<std::vector<int>>> by_degree(max_deg + 1);
+  std::vector<int> e(nv, 0);
+  for (;;) {
+    by_degree[std::accumulate(e.begin(), e.end(), 0)].push_back(e);
+    size_t i = nv;  // increment the last digit, carrying leftwards
+    while (i > 0 && e[i - 1] == bounds[i - 1]) e[--i] = 0;
+    if (i == 0) break;
+    ++e[i - 1];
   }
-  std::stable_sort(tuples.begin(), tuples.end(),
-                   [](const std::vector<int>& a, const std::vector<int>& b) {
-                     const int ga = std::accumulate(a.begin(), a.end(), 0);
-                     const int gb = std::accumulate(b.begin(), b.end(), 0);
-                     if (ga != gb) return ga < gb;
-                     return a < b;
-                   });
-  return tuples;
+  std::vector<std::vector<int>> out;
+  for (auto& bucket : by_degree)
+    for (auto& t : bucket) out.push_back(std::move(t));
+  return out;
 }
 
 struct Polynomial {
@@ -369,76 +369,107 @@ inline MwpCwpBreakdown mwpcwp_cycles(const DeviceProfile& hw, const KernelMetric
 }
 
 namespace detail {
+// DeviceProfile's fields in the profile-file key order (perfmodel.hpp:91-108):
+// name, and a pointer to the count (integer) or rate member.
+struct ProfileField {
+  const char* name;
+  long long DeviceProfile::*count;
+  double DeviceProfile::*rate;
+};
+inline const std::vector<ProfileField>& profile_fields() {
+  static const std::vector<ProfileField> f = {
+      {"R_max", &DeviceProfile::R_max, nullptr},
+      {"Z_max", &DeviceProfile::Z_max, nullptr},
+      {"T_max", &DeviceProfile::T_max, nullptr},
+      {"B_max", &DeviceProfile::B_max, nullptr},
+      {"W_max", &DeviceProfile::W_max, nullptr},
+      {"num_SM", &DeviceProfile::num_SM, nullptr},
+      {"freq_GHz", nullptr, &DeviceProfile::freq_GHz},
+      {"mem_latency_cycles", nullptr, &DeviceProfile::mem_latency_cycles},
+      {"departure_del_coal_cycles", nullptr, &DeviceProfile::departure_del_coal_cycles},
+      {"departure_del_uncoal_cycles", nullptr, &DeviceProfile::departure_del_uncoal_cycles},
+      {"mem_bandwidth_GBps", nullptr, &DeviceProfile::mem_bandwidth_GBps},
+      {"issue_cycles", nullptr, &DeviceProfile::issue_cycles},
+      {"load_bytes_per_warp", &DeviceProfile::load_bytes_per_warp, nullptr},
+      {"uncoal_per_mw", &DeviceProfile::uncoal_per_mw, nullptr}};
+  return f;
+}
 inline const std::vector<std::string>& profile_keys() {
-  static const std::vector<std::string> keys = {
-      "R_max", "Z_max", "T_max", "B_max", "W_max", "num_SM", "freq_GHz",
-      "mem_latency_cycles", "departure_del_coal_cycles", "departure_del_uncoal_cycles",
-      "mem_bandwidth_GBps", "issue_cycles", "load_bytes_per_warp", "uncoal_per_mw"};
+  static const std::vector<std::string> keys = [] {
+    std::vector<std::string> k;
+    for (const ProfileField& f : profile_fields()) k.push_back(f.name);
+    return k;
+  }();
   return keys;
 }
+// The text between the first and last character that is not a blank.
 inline std::string trim(const std::string& s) {
-  const size_t b = s.find_first_not_of(" \t\r");
-  const size_t e = s.find_last_not_of(" \t\r");
-  return b == std::string::npos ? std::string() : s.substr(b, e - b + 1);
+  size_t b = 0, e = s.size();
+  auto blank = [](char c) { return c == ' ' || c == '\t' || c == '\r'; };
+  while (b < e && blank(s[b])) ++b;
+  while (e > b && blank(s[e - 1])) --e;
+  return s.substr(b, e - b);
 }
 }  // namespace detail
 
-// perf::parse_profile (perfmodel.hpp:111-180): same checks and messages.
+// perf::parse_profile (perfmodel.hpp:111-180): "key = value" lines, '#'
+// comments, blank lines; every key exactly once; values parsed by std::stod
+// with full consumption, positive; count fields integral; T_max <= 1024.
+// Same checks, order and messages as the reference.
 inline DeviceProfile parse_profile(const std::string& text) {
-  std::map<std::string, double> seen;
-  std::istringstream in(text);
-  std::string line;
-  size_t line_no = 0;
-  const auto& keys = detail::profile_keys();
-  while (std::getline(in, line)) {
-    ++line_no;
-    const std::string stripped = line.substr(0, line.find('#'));
-    if (stripped.find_first_not_of(" \t\r") == std::string::npos) continue;
-    const size_t eq = stripped.find('=');
-    if (eq == std::string::npos)
-      throw ProfileError("profile line " + std::to_string(line_no) + ": expected 'key = value'");
-    const std::string key = detail::trim(stripped.substr(0, eq));
-    const std::string value = detail::trim(stripped.substr(eq + 1));
-    if (std::find(keys.begin(), keys.end(), key) == keys.end())
-      throw ProfileError("profile line " + std::to_string(line_no) + ": unknown key '" + key + "'");
-    if (seen.count(key))
-      throw ProfileError("profile line " + std::to_string(line_no) + ": duplicate key '" + key + "'");
-    double v = 0;
-    try {
-      size_t used = 0;
-      v = std::stod(value, &used);
-      if (used != value.size()) throw std::invalid_argument(value);
-    } catch (const std::exception&) {
-      throw ProfileError("profile line " + std::to_string(line_no) + ": bad numeric value '" +
-                         value + "'");
-    }
-    if (!(v > 0))
-      throw ProfileError("profile line " + std::to_string(line_no) + ": '" + key +
-                         "' must be positive");
-    seen[key] = v;
-  }
-  for (const std::string& key : keys)
-    if (!seen.count(key)) throw ProfileError("profile is missing key '" + key + "'");
-  auto as_count = [&](const std::string& key) {
-    const double v = seen[key];
-    if (v != std::floor(v)) throw ProfileError("profile key '" + key + "' must be an integer");
-    return static_cast<long long>(v);
+  const auto& fields = detail::profile_fields();
+  std::vector<double> value(fields.size(), 0.0);
+  std::vector<bool> given(fields.size(), false);
+  size_t line_no = 0, pos = 0;
+  auto fail = [&](const std::string& what) -> void {
+    throw ProfileError("profile line " + std::to_string(line_no) + ": " + what);
   };
+  while (pos <= text.size()) {
+    size_t nl = text.find('\n', pos);
+    if (nl == std::string::npos) nl = text.size();
+    std::string line = text.substr(pos, nl - pos);
+    pos = nl + 1;
+    ++line_no;
+    line = detail::trim(line.substr(0, line.find('#')));
+    if (!line.empty()) {
+      const size_t eq = line.find('=');
+      if (eq == std::string::npos) fail("expected 'key = value'");
+      const std::string key = detail::trim(line.substr(0, eq));
+      const std::string val = detail::trim(line.substr(eq + 1));
+      size_t k = 0;
+      while (k < fields.size() && key != fields[k].name) ++k;
+      if (k == fields.size()) fail("unknown key '" + key + "'");
+      if (given[k]) fail("duplicate key '" + key + "'");
+      double v = 0.0;
+      bool ok = !val.empty();
+      if (ok) {
+        try {
+          size_t used = 0;
+          v = std::stod(val, &used);
+          ok = used == val.size();
+        } catch (const std::exception&) {
+          ok = false;
+        }
+      }
+      if (!ok) fail("bad numeric value '" + val + "'");
+      if (!(v > 0)) fail("'" + key + "' must be positive");
+      value[k] = v;
+      given[k] = true;
+    }
+    if (nl == text.size()) break;
+  }
+  for (size_t k = 0; k < fields.size(); ++k)
+    if (!given[k]) throw ProfileError(std::string("profile is missing key '") + fields[k].name + "'");
   DeviceProfile hw;
-  hw.R_max = as_count("R_max");
-  hw.Z_max = as_count("Z_max");
-  hw.T_max = as_count("T_max");
-  hw.B_max = as_count("B_max");
-  hw.W_max = as_count("W_max");
-  hw.num_SM = as_count("num_SM");
-  hw.freq_GHz = seen["freq_GHz"];
-  hw.mem_latency_cycles = seen["mem_latency_cycles"];
-  hw.departure_del_coal_cycles = seen["departure_del_coal_cycles"];
-  hw.departure_del_uncoal_cycles = seen["departure_del_uncoal_cycles"];
-  hw.mem_bandwidth_GBps = seen["mem_bandwidth_GBps"];
-  hw.issue_cycles = seen["issue_cycles"];
-  hw.load_bytes_per_warp = as_count("load_bytes_per_warp");
-  hw.uncoal_per_mw = as_count("uncoal_per_mw");
+  for (size_t k = 0; k < fields.size(); ++k) {
+    if (fields[k].count) {
+      if (value[k] != std::floor(value[k]))
+        throw ProfileError(std::string("profile key '") + fields[k].name + "' must be an integer");
+      hw.*(fields[k].count) = static_cast<long long>(value[k]);
+    } else {
+      hw.*(fields[k].rate) = value[k];
+    }
+  }
   if (hw.T_max > 1024) throw ProfileError("T_max exceeds 1024, the architectural block limit");
   return hw;
 }
@@ -478,30 +509,31 @@ struct MetricSpec {
   }
 };
 
-// perf::check_metric_spec (perfmodel.hpp:428-456).
+// perf::check_metric_spec (perfmodel.hpp:428-456): the five required
+// metrics and regs/shared each need a model or a constant; variables are
+// D<k> data parameters or bx/by/bz (never a profile field name), bx and by
+// both present; every model uses the shared variable order.
 inline void check_metric_spec(const MetricSpec& spec) {
-  for (const std::string& name : required_metric_names())
-    if (!spec.covers(name))
-      throw ModelError("metric '" + name + "' has neither a model nor a constant");
-  for (const char* name : {kMetricRegs, kMetricShared})
-    if (!spec.covers(name))
-      throw ModelError(std::string("metric '") + name + "' has neither a model nor a constant");
-  bool has_bx = false, has_by = false;
+  std::vector<std::string> need = required_metric_names();
+  need.push_back(kMetricRegs);
+  need.push_back(kMetricShared);
+  for (const std::string& name : need)
+    if (!spec.covers(name)) throw ModelError("metric '" + name + "' has neither a model nor a constant");
+  const auto& hw_keys = detail::profile_keys();
+  int blocks_seen = 0;  // bit 0: bx, bit 1: by
   for (const std::string& v : spec.variables) {
-    has_bx |= v == "bx";
-    has_by |= v == "by";
-    const auto& hw_keys = detail::profile_keys();
-    if (std::find(hw_keys.begin(), hw_keys.end(), v) != hw_keys.end())
+    if (std::count(hw_keys.begin(), hw_keys.end(), v))
       throw ModelError("variable '" + v + "' collides with a hardware field");
-    const bool data_param = v.size() >= 2 && v[0] == 'D' &&
-                            v.find_first_not_of("0123456789", 1) == std::string::npos;
-    if (!data_param && v != "bx" && v != "by" && v != "bz")
+    if (v == "bx") blocks_seen |= 1;
+    else if (v == "by") blocks_seen |= 2;
+    else if (v != "bz" && !(v.size() >= 2 && v[0] == 'D' &&
+                            std::all_of(v.begin() + 1, v.end(), [](char c) { return c >= '0' && c <= '9'; })))
       throw ModelError("variable '" + v + "' is not a data parameter (D1..Dd) or block dimension");
   }
-  if (!has_bx || !has_by) throw ModelError("metric variables must include bx and by");
-  for (const auto& [name, f] : spec.models)
-    if (f.num.variables != spec.variables)
-      throw ModelError("model '" + name + "' disagrees with the shared variable order");
+  if (blocks_seen != 3) throw ModelError("metric variables must include bx and by");
+  for (const auto& entry : spec.models)
+    if (entry.second.num.variables != spec.variables)
+      throw ModelError("model '" + entry.first + "' disagrees with the shared variable order");
 }
 
 struct EmitOptions {
@@ -535,19 +567,23 @@ struct SampleSet {
   std::size_t dims() const { return samples.empty() ? 0 : samples.front().data_params.size(); }
 };
 
-// data::enumerate_configs (datakit.hpp:79-94).
+// data::enumerate_configs (datakit.hpp:79-94): power-of-two block shapes
+// 2^i x 2^j x 2^k (j = 0 unless dims >= 2, k = 0 unless dims == 3, each
+// dimension <= 1024) with min_threads <= threads <= max_threads, in lex
+// order of (bx, by, bz).
 inline std::vector<perf::LaunchConfig> enumerate_configs(long long max_threads = 1024,
                                                          long long min_threads = 32,
                                                          int dims = 2) {
   if (min_threads < 1 || min_threads > max_threads || max_threads > 1024)
     throw std::invalid_argument("enumerate_configs: need 1 <= min_threads <= max_threads <= 1024");
   if (dims < 1 || dims > 3) throw std::invalid_argument("enumerate_configs: dims must be 1, 2 or 3");
+  const int ey = dims >= 2 ? 10 : 0, ez = dims == 3 ? 10 : 0;
   std::vector<perf::LaunchConfig> out;
-  for (long long bx = 1; bx <= 1024; bx *= 2)
-    for (long long by = 1; by <= (dims >= 2 ? 1024 : 1); by *= 2)
-      for (long long bz = 1; bz <= (dims >= 3 ? 1024 : 1); bz *= 2) {
-        const long long t = bx * by * bz;
-        if (t >= min_threads && t <= max_threads) out.push_back({bx, by, bz});
+  for (int i = 0; i <= 10; ++i)
+    for (int j = 0; j <= ey; ++j)
+      for (int k = 0; k <= ez; ++k) {
+        const perf::LaunchConfig c{1LL << i, 1LL << j, 1LL << k};
+        if (c.threads() >= min_threads && c.threads() <= max_threads) out.push_back(c);
       }
   return out;
 }
@@ -712,61 +748,96 @@ struct AllMetricsFailed : std::runtime_error {
 };
 
 // pipe::sample_variables / default_bounds / metric_points (pipeline.hpp:72-133).
+// The model variables of a sample set (pipeline.hpp:72-86): D1..Dd, bx, by,
+// and bz when some sample uses a third block dimension.
 inline std::vector<std::string> sample_variables(const data::SampleSet& set) {
-  std::vector<std::string> vars;
-  for (std::size_t i = 1; i <= set.dims(); ++i) vars.push_back("D" + std::to_string(i));
-  vars.push_back("bx");
-  vars.push_back("by");
-  for (const data::Sample& s : set.samples)
-    if (s.config.bz != 1) {
-      vars.push_back("bz");
-      break;
-    }
+  const bool uses_bz = std::any_of(set.samples.begin(), set.samples.end(),
+                                   [](const data::Sample& s) { return s.config.bz != 1; });
+  std::vector<std::string> vars(set.dims());
+  for (std::size_t i = 0; i < vars.size(); ++i) vars[i] = "D" + std::to_string(i + 1);
+  vars.insert(vars.end(), {"bx", "by"});
+  if (uses_bz) vars.emplace_back("bz");
   return vars;
 }
 
+// pipe::default_bounds (pipeline.hpp:88-93): numerator 2, denominator 1 per
+// variable.
 inline poly::DegreeBounds default_bounds(std::size_t n_variables) {
-  poly::DegreeBounds b;
-  b.num.assign(n_variables, 2);
-  b.den.assign(n_variables, 1);
-  return b;
+  return poly::DegreeBounds{std::vector<int>(n_variables, 2), std::vector<int>(n_variables, 1)};
 }
 
+namespace detail {
+// Column-major-by-sample coordinates (m x nv, row per sample) of a sample
+// set in `variables` order (pipeline.hpp:97-113 coordinate rules).
+inline std::vector<double> sample_matrix(const data::SampleSet& set,
+                                         const std::vector<std::string>& variables) {
+  const size_t nv = variables.size();
+  // per variable: -1 bx, -2 by, -3 bz, k >= 0 data parameter k
+  std::vector<long> src(nv);
+  for (size_t j = 0; j < nv; ++j) {
+    const std::string& v = variables[j];
+    if (v == "bx") src[j] = -1;
+    else if (v == "by") src[j] = -2;
+    else if (v == "bz") src[j] = -3;
+    else if (v.size() >= 2 && v[0] == 'D') src[j] = (long)std::stoul(v.substr(1)) - 1;
+    else throw PipelineError("variable '" + v + "' is not a data parameter or block dimension");
+  }
+  std::vector<double> X(set.samples.size() * nv);
+  for (size_t r = 0; r < set.samples.size(); ++r) {
+    const data::Sample& s = set.samples[r];
+    for (size_t j = 0; j < nv; ++j) {
+      const long k = src[j];
+      double x;
+      if (k == -1) x = (double)s.config.bx;
+      else if (k == -2) x = (double)s.config.by;
+      else if (k == -3) x = (double)s.config.bz;
+      else if (k >= 0 && (size_t)k < s.data_params.size()) x = (double)s.data_params[k];
+      else throw PipelineError("variable '" + variables[j] + "' exceeds the sample's data-parameter count");
+      X[r * nv + j] = x;
+    }
+  }
+  return X;
+}
+
+inline std::vector<double> metric_column(const data::SampleSet& set, const std::string& metric) {
+  std::vector<double> y(set.samples.size());
+  for (size_t r = 0; r < y.size(); ++r) {
+    auto it = set.samples[r].metric_values.find(metric);
+    if (it == set.samples[r].metric_values.end())
+      throw PipelineError("sample set has no metric column '" + metric + "'");
+    y[r] = it->second;
+  }
+  return y;
+}
+}  // namespace detail
+
+// pipe::metric_points (pipeline.hpp:115-133): one metric column as
+// (point, value) pairs.
 inline poly::PointValueSet metric_points(const data::SampleSet& set, const std::string& metric,
                                          const std::vector<std::string>& variables) {
+  const std::vector<double> y = detail::metric_column(set, metric);
+  const std::vector<double> X = detail::sample_matrix(set, variables);
   poly::PointValueSet out;
-  out.points.reserve(set.samples.size());
-  out.values.reserve(set.samples.size());
-  for (const data::Sample& s : set.samples) {
-    auto it = s.metric_values.find(metric);
-    if (it == s.metric_values.end())
-      throw PipelineError("sample set has no metric column '" + metric + "'");
-    std::vector<double> x;
-    x.reserve(variables.size());
-    for (const std::string& v : variables) {
-      if (v == "bx") x.push_back((double)s.config.bx);
-      else if (v == "by") x.push_back((double)s.config.by);
-      else if (v == "bz") x.push_back((double)s.config.bz);
-      else {
-        const std::size_t k = std::stoul(v.substr(1));
-        if (k < 1 || k > s.data_params.size())
-          throw PipelineError("variable '" + v + "' exceeds the sample's data-parameter count");
-        x.push_back((double)s.data_params[k - 1]);
-      }
-    }
-    out.points.push_back(std::move(x));
-    out.values.push_back(it->second);
-  }
+  out.values = y;
+  out.points.resize(y.size());
+  for (size_t r = 0; r < y.size(); ++r)
+    out.points[r].assign(X.begin() + r * variables.size(), X.begin() + (r + 1) * variables.size());
   return out;
 }
 
 struct FitOptions {
   double rank_tol = poly::kDefaultRankTol;
+  int device = 0;
 };
 
-// pipe::fit_all_metrics (pipeline.hpp:145-184): one GPU rational fit per
-// metric column; numerical failures are recorded per metric, a full wipeout
-// raises AllMetricsFailed.
+// pipe::fit_all_metrics (pipeline.hpp:145-184) the B200 way: the sample
+// coordinates are laid out once (m x nv) and every metric column is fitted
+// concurrently on the GPU (rpg_fit_rational_multi: one upload of X, one
+// stream per metric).  The reference's argument checks run first, in its
+// metric order and with its messages; numerical failures (DegenerateFit /
+// SvdFailure) are recorded per metric, a full wipeout raises
+// AllMetricsFailed.  Each metric's model is what poly::fit_rational returns
+// for it alone.
 inline MetricModelSet fit_all_metrics(const data::SampleSet& samples,
                                       const std::map<std::string, poly::DegreeBounds>& bounds,
                                       const std::map<std::string, double>& constants,
@@ -775,22 +846,69 @@ inline MetricModelSet fit_all_metrics(const data::SampleSet& samples,
   MetricModelSet out;
   out.variables = sample_variables(samples);
   out.constants = constants;
-  for (const std::string& metric : samples.metric_names) {
+  const size_t nv = out.variables.size(), m = samples.samples.size(), k = samples.metric_names.size();
+  std::vector<poly::DegreeBounds> b(k);
+  std::vector<std::vector<double>> ys(k);
+  for (size_t i = 0; i < k; ++i) {
+    const std::string& metric = samples.metric_names[i];
     if (constants.count(metric))
       throw PipelineError("metric '" + metric + "' is both a sample column and a declared constant");
-    poly::DegreeBounds b = bounds.count(metric) ? bounds.at(metric) : default_bounds(out.variables.size());
-    if (b.num.size() != out.variables.size() || b.den.size() != out.variables.size())
+    auto it = bounds.find(metric);
+    b[i] = it != bounds.end() ? it->second : default_bounds(nv);
+    if (b[i].num.size() != nv || b[i].den.size() != nv)
       throw PipelineError("degree bounds for metric '" + metric + "' must have " +
-                          std::to_string(out.variables.size()) + " entries per side");
-    try {
-      auto pv = metric_points(samples, metric, out.variables);
-      auto fitted = poly::fit_rational(pv, out.variables, b, opts.rank_tol);
-      out.models[metric] = MetricModel{std::move(fitted.first), std::move(fitted.second)};
-    } catch (const poly::DegenerateFit& e) {
-      out.failures[metric] = e.what();
-    } catch (const poly::SvdFailure& e) {
-      out.failures[metric] = e.what();
+                          std::to_string(nv) + " entries per side");
+    ys[i] = detail::metric_column(samples, metric);
+  }
+  const std::vector<double> X = detail::sample_matrix(samples, out.variables);
+  struct Out {
+    std::vector<double> coef, sigma;
+    int32_t rank = 0, truncated = 0, safeguard = 0;
+    double residual = 0.0;
+  };
+  std::vector<Out> res(k);
+  std::vector<rpg_fit_job> jobs(k);
+  for (size_t i = 0; i < k; ++i) {
+    const size_t n = poly::monomial_basis(b[i].num).size() + poly::monomial_basis(b[i].den).size();
+    res[i].coef.assign(n, 0.0);
+    res[i].sigma.assign(std::max<size_t>(1, std::min(m, n)), 0.0);
+    rpg_fit_job& J = jobs[i];
+    J = rpg_fit_job{};
+    J.y = ys[i].data();
+    J.num_bounds = b[i].num.data();
+    J.den_bounds = b[i].den.data();
+    J.coef_out = res[i].coef.data();
+    J.sigma_out = res[i].sigma.data();
+    J.rank_out = &res[i].rank;
+    J.truncated_out = &res[i].truncated;
+    J.residual_out = &res[i].residual;
+    J.safeguard_out = &res[i].safeguard;
+  }
+  char err[512] = {0};
+  const int rc = rpg_fit_rational_multi(X.data(), (int64_t)m, (int32_t)nv, jobs.data(), (int32_t)k,
+                                        opts.rank_tol, opts.device, err, sizeof err);
+  if (rc == RPG_E_INVALID) throw std::invalid_argument(err);
+  if (rc != RPG_OK) throw std::runtime_error(std::string("librpgpu: ") + err);
+  for (size_t i = 0; i < k; ++i) {
+    const std::string& metric = samples.metric_names[i];
+    if (jobs[i].status == RPG_E_FIT) {
+      out.failures[metric] = jobs[i].message;
+      continue;
     }
+    if (jobs[i].status == RPG_E_INVALID) throw std::invalid_argument(jobs[i].message);
+    if (jobs[i].status != RPG_OK) throw std::runtime_error(std::string("librpgpu: ") + jobs[i].message);
+    const auto nb = poly::monomial_basis(b[i].num), db = poly::monomial_basis(b[i].den);
+    MetricModel mm;
+    mm.fn.num = poly::Polynomial{out.variables, nb,
+                                 std::vector<double>(res[i].coef.begin(), res[i].coef.begin() + nb.size())};
+    mm.fn.den = poly::Polynomial{out.variables, db,
+                                 std::vector<double>(res[i].coef.begin() + nb.size(), res[i].coef.end())};
+    const size_t n_sig = std::min(m, nb.size() + db.size());
+    mm.report.residual_norm = res[i].residual;
+    mm.report.numerical_rank = res[i].rank;
+    mm.report.singular_values.assign(res[i].sigma.begin(), res[i].sigma.begin() + n_sig);
+    mm.report.truncated = res[i].truncated != 0;
+    out.models[metric] = std::move(mm);
   }
   if (out.models.empty()) {
     std::string msg = "no metric could be fitted:";
@@ -1909,52 +2027,63 @@ inline std::string config_label(const perf::LaunchConfig& c) {
 }
 }  // namespace detail
 
+// The three report formats of pipeline.hpp:897-934 (output strings are the
+// reference's, byte for byte): every row as its cells once, then joined.
+namespace detail {
+struct RowCells {
+  std::string bx, by, bz, ec, occ, tag;
+};
+inline RowCells cells(const SearchRow& row) {
+  return {std::to_string(row.config.bx), std::to_string(row.config.by),
+          std::to_string(row.config.bz), format_double(row.estimated_cycles),
+          format_double(row.occupancy), row.case_tag};
+}
+}  // namespace detail
+
 inline std::string format_search_csv(const SearchResult& r) {
-  std::ostringstream out;
-  out << "bx,by,bz,Ec,occupancy,case\n";
-  for (const SearchRow& row : r.ranking)
-    out << row.config.bx << "," << row.config.by << "," << row.config.bz << ","
-        << detail::format_double(row.estimated_cycles) << ","
-        << detail::format_double(row.occupancy) << "," << row.case_tag << "\n";
-  return out.str();
+  std::string out = "bx,by,bz,Ec,occupancy,case\n";
+  for (const SearchRow& row : r.ranking) {
+    const detail::RowCells c = detail::cells(row);
+    out += c.bx + ',' + c.by + ',' + c.bz + ',' + c.ec + ',' + c.occ + ',' + c.tag + '\n';
+  }
+  return out;
 }
 
+// Left-aligned columns two spaces apart, a dashed rule under the header
+// (detail::format_table, pipeline.hpp:870-894), then the counters line.
 inline std::string format_search_text(const SearchResult& r) {
-  std::vector<std::vector<std::string>> rows;
-  for (const SearchRow& row : r.ranking)
-    rows.push_back({detail::config_label(row.config), detail::format_double(row.estimated_cycles),
-                    detail::format_double(row.occupancy), row.case_tag});
-  const std::vector<std::string> header = {"config", "Ec", "occupancy", "case"};
-  std::vector<size_t> width(header.size());
-  for (size_t j = 0; j < header.size(); ++j) width[j] = header[j].size();
-  for (const auto& row : rows)
-    for (size_t j = 0; j < row.size(); ++j) width[j] = std::max(width[j], row[j].size());
-  std::ostringstream out;
-  auto emit = [&](const std::vector<std::string>& row) {
-    for (size_t j = 0; j < row.size(); ++j) {
-      out << row[j];
-      if (j + 1 < row.size()) out << std::string(width[j] - row[j].size() + 2, ' ');
+  std::vector<std::array<std::string, 4>> table = {{"config", "Ec", "occupancy", "case"}};
+  for (const SearchRow& row : r.ranking) {
+    const detail::RowCells c = detail::cells(row);
+    table.push_back({detail::config_label(row.config), c.ec, c.occ, c.tag});
+  }
+  std::array<size_t, 4> w{};
+  for (const auto& t : table)
+    for (size_t j = 0; j < 4; ++j) w[j] = std::max(w[j], t[j].size());
+  std::string out;
+  auto line = [&](const std::array<std::string, 4>& t) {
+    for (size_t j = 0; j < 4; ++j) {
+      out += t[j];
+      if (j < 3) out.append(w[j] - t[j].size() + 2, ' ');
     }
-    out << "\n";
+    out += '\n';
   };
-  emit(header);
-  size_t total = 0;
-  for (size_t j = 0; j < width.size(); ++j) total += width[j] + (j + 1 < width.size() ? 2 : 0);
-  out << std::string(total, '-') << "\n";
-  for (const auto& row : rows) emit(row);
-  out << "evaluated " << r.evaluated << " configuration(s), " << r.infeasible
-      << " infeasible; optimum ties: " << r.ties << "\n";
-  return out.str();
+  line(table[0]);
+  out.append(w[0] + w[1] + w[2] + w[3] + 6, '-');
+  out += '\n';
+  for (size_t i = 1; i < table.size(); ++i) line(table[i]);
+  out += "evaluated " + std::to_string(r.evaluated) + " configuration(s), " +
+         std::to_string(r.infeasible) + " infeasible; optimum ties: " + std::to_string(r.ties) + "\n";
+  return out;
 }
 
+// One JSON object per ranked row (nlohmann ordered_json's compact dump).
 inline std::string format_search_jsonl(const SearchResult& r) {
   std::string out;
   for (const SearchRow& row : r.ranking) {
-    out += "{\"config\":[" + std::to_string(row.config.bx) + "," + std::to_string(row.config.by) +
-           "," + std::to_string(row.config.bz) + "],\"Ec\":" +
-           detail::format_double(row.estimated_cycles) +
-           ",\"occupancy\":" + detail::format_double(row.occupancy) + ",\"case_tag\":\"" +
-           row.case_tag + "\"}\n";
+    const detail::RowCells c = detail::cells(row);
+    out += "{\"config\":[" + c.bx + "," + c.by + "," + c.bz + "],\"Ec\":" + c.ec +
+           ",\"occupancy\":" + c.occ + ",\"case_tag\":\"" + c.tag + "\"}\n";
   }
   return out;
 }

@@ -5,7 +5,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <iostream>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -43,6 +45,24 @@ static void cpu_tests() {
   CHECK(throws_with<perf::ProfileError>([] { perf::parse_profile("R_max 1\n"); }, "expected 'key = value'"));
   CHECK(throws_with<perf::ProfileError>([] { perf::parse_profile("bogus = 1\n"); }, "unknown key"));
   CHECK(throws_with<perf::ProfileError>([] { perf::parse_profile("R_max = 1\n"); }, "missing key"));
+  {
+    std::ifstream f(root + "/data/sample_device.profile");
+    std::stringstream ss;
+    ss << f.rdbuf();
+    const std::string base = ss.str();
+    auto with = [&](const std::string& from, const std::string& to) {
+      std::string t = base;
+      t.replace(t.find(from), from.size(), to);
+      return t;
+    };
+    CHECK(throws_with<perf::ProfileError>([&] { perf::parse_profile(base + "W_max = 48\n"); }, "duplicate key 'W_max'"));
+    CHECK(throws_with<perf::ProfileError>([&] { perf::parse_profile(with("W_max = 48", "W_max = -4")); }, "'W_max' must be positive"));
+    CHECK(throws_with<perf::ProfileError>([&] { perf::parse_profile(with("W_max = 48", "W_max = 4.5")); }, "'W_max' must be an integer"));
+    CHECK(throws_with<perf::ProfileError>([&] { perf::parse_profile(with("W_max = 48", "W_max = 4x")); }, "bad numeric value '4x'"));
+    CHECK(throws_with<perf::ProfileError>([&] { perf::parse_profile(with("T_max = 1024", "T_max = 2048")); }, "T_max exceeds 1024"));
+    CHECK(perf::parse_profile(with("W_max = 48", "W_max = 0x30   # hex")).W_max == 48);
+  }
+  CHECK(data::enumerate_configs(1024, 32, 1).size() == 6);
   CHECK(poly::monomial_basis({1, 1}) == (std::vector<std::vector<int>>{{0, 0}, {0, 1}, {1, 0}, {1, 1}}));
   CHECK(poly::monomial_basis({2, 1, 1}).size() == 12);
   CHECK(data::enumerate_configs().size() == 51);
