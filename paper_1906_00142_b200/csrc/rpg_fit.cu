@@ -33,6 +33,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <map>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -818,19 +820,27 @@ den_pass(const FitParams F, const double* __restrict__ cd, const double* __restr
   den_pass_body<NDT>(F, cd, dd, alphas, n_alpha, newton, partial, src);
 }
 
+// Folds G per-block partials (W values each) into out: one thread per
+// value, the G loads of a thread independent of each other (issued back to
+// back, one L2 round trip for the whole fold instead of one per value), a
+// fixed g order (deterministic).
 __device__ __forceinline__ void den_pass_reduce(const double* __restrict__ partial, int G, int nd,
                                                 double* __restrict__ out) {
   const int W = 2 * kAlphas + nd + nd * nd;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int e = warp; e < W; e += nw) {
+  for (int e = threadIdx.x; e < W; e += blockDim.x) {
     const bool is_min = e < 2 * kAlphas && (e % 2) == 0;
     double t = is_min ? INFINITY : 0.0;
-    for (int g = lane; g < G; g += 32) t = is_min ? fmin(t, partial[(size_t)g * W + e]) : t + partial[(size_t)g * W + e];
-    for (int o = 16; o > 0; o >>= 1) {
-      const double u = __shfl_xor_sync(0xffffffffu, t, o);
-      t = is_min ? fmin(t, u) : t + u;
+    const double* p = partial + e;
+    int g = 0;
+    for (; g + 8 <= G; g += 8) {
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = p[(size_t)(g + i) * W];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t = is_min ? fmin(t, v[i]) : t + v[i];
     }
-    if (lane == 0) out[e] = t;
+    for (; g < G; ++g) t = is_min ? fmin(t, p[(size_t)g * W]) : t + p[(size_t)g * W];
+    out[e] = t;
   }
 }
 
@@ -977,22 +987,17 @@ __device__ __forceinline__ double warp_sum(double t) {
   return t;
 }
 
-// rows[i] = (R S (c + alpha dc))[i] = sum_{k >= i} R[i][k] S[k] (c[k] + alpha
-// dc[k]), one warp per row, lanes over k, a fixed shuffle tree — the same
-// bits for the Newton step's phi0 (alpha = 0, dc = null) and the line
-// search's candidates.
-__device__ __forceinline__ void rs_rows(const double* R, const double* __restrict__ S,
-                                        const double* __restrict__ c, const double* __restrict__ dc,
-                                        double alpha, int n, double* rows, int warp0, int nwarps) {
-  const int warp = (int)(threadIdx.x >> 5) - warp0, lane = threadIdx.x & 31;
-  if (warp < 0 || warp >= nwarps) return;
-  for (int i = warp; i < n; i += nwarps) {
-    double t = 0.0;
-    for (int k = i + lane; k < n; k += 32)
-      t = fma(R[i * n + k], S[k] * (dc ? c[k] + alpha * dc[k] : c[k]), t);
-    t = warp_sum(t);
-    if (lane == 0) rows[i] = t;
-  }
+// rows[i] = (R v)[i] = sum_{k >= i} R[i][k] v[k] for the upper-triangular
+// R, one thread per row (thread `first` + i), k ascending — the same bits
+// for the Newton step's phi0 (v = S c) and the line search's candidates
+// (v = S (c + alpha dc)), whichever thread computes a row.
+__device__ __forceinline__ void r_rows(const double* R, const double* v, int n, double* rows,
+                                       int first) {
+  const int i = (int)threadIdx.x - first;
+  if (i < 0 || i >= n) return;
+  double t = 0.0;
+  for (int k = i; k < n; ++k) t = fma(R[i * n + k], v[k], t);
+  rows[i] = t;
 }
 
 // sum_i rows[i]^2 over n <= 64 rows: one warp, lanes i and i + 32, then the
@@ -1080,7 +1085,10 @@ __device__ void newton_schur_fast(const double* R, const double* __restrict__ S,
   const double* B = Ainv + nn * nn;
   const double* Fm = B + nn * nd;
   const double* Sv0 = Fm + nn * nd;
-  rs_rows(R, S, c, nullptr, 0.0, n, RSc, 0, nw);
+  double* cv = ws + 224;      // 64: S .* c
+  for (int k = threadIdx.x; k < n; k += blockDim.x) cv[k] = S[k] * c[k];
+  __syncthreads();
+  r_rows(R, cv, n, RSc, 0);
   __syncthreads();
   for (int k = warp; k < n; k += nw) {
     double t = 0.0;
@@ -1444,15 +1452,17 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int na = ctl->n_alpha;
   __shared__ double rows[kAlphas][kMaxCols];
-  // ||R S cn||^2 per candidate: the rows as the Newton step's phi0 forms
-  // them (rs_rows: the same bits per row whichever warp computes it), two
-  // warps per candidate, then the fixed-order sum of squares.
-  {
-    const int nw = blockDim.x >> 5, per = nw / kAlphas > 0 ? nw / kAlphas : 1;
-    for (int a = 0; a < na; ++a)
-      if (warp / per == a || (per == 0 && warp == a))
-        rs_rows(R, S, c, dc, ctl->al[a], n, rows[a], a * per, per);
+  // ||R S cn||^2 per candidate: the candidate vectors S (c + alpha dc),
+  // their rows (r_rows: the Newton step's phi0 rows for alpha = 0), then the
+  // fixed-order sum of squares (sumsq_rows) — one thread per (candidate, k)
+  // and per (candidate, row).
+  __shared__ double cvs[kAlphas][kMaxCols];
+  for (int e = threadIdx.x; e < na * n; e += blockDim.x) {
+    const int a = e / n, k = e % n;
+    cvs[a][k] = S[k] * (c[k] + ctl->al[a] * dc[k]);
   }
+  __syncthreads();
+  for (int a = 0; a < na; ++a) r_rows(R, cvs[a], n, rows[a], a * n);
   __syncthreads();
   if (warp < na) {
     const double acc = sumsq_rows(rows[warp], n);
@@ -1668,6 +1678,22 @@ cudaError_t fit_malloc(void** p, size_t bytes) {
   return g_fit_stream ? cudaMallocAsync(p, bytes, g_fit_stream) : cudaMalloc(p, bytes);
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only ever raised, under a
+// lock: concurrent fits (rpg_fit_rational_multi) with different column
+// counts must not lower the limit under another thread's launch.
+cudaError_t raise_smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> cur;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[{fn, dev}];
+  if (bytes <= c) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) c = bytes;
+  return e;
+}
+
 struct DevBuf {
   void* p = nullptr;
   ~DevBuf() {
@@ -1697,7 +1723,7 @@ int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, c
   const int64_t tiles = (F.m + kTile - 1) / kTile;
   const size_t sm1 = tsqr_smem(ncols);
   int per_sm = 1;
-  FCUDA(cudaFuncSetAttribute(tsqr_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(tsqr_tiles), sm1));
   FCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_tiles, kFitThreads, sm1));
   (void)per_sm;
   int G = (int)std::min<int64_t>(tiles, 4LL * sms);
@@ -1706,7 +1732,7 @@ int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, c
   tsqr_tiles<<<G, kFitThreads, sm1, s>>>(F, Rbuf->as<double>());
   FCUDA(cudaGetLastError());
   const size_t sm2 = sizeof(double) * ((size_t)kCombine * ncols * ncols + 32 + kMaxCols);
-  FCUDA(cudaFuncSetAttribute(tsqr_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(tsqr_combine), sm2));
   // Tree over the G factors, one launch per level, ping-ponging between
   // Rbuf and tmp; the root ends in Rbuf.
   int count = G;
@@ -1760,10 +1786,10 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
   }
   const size_t sm = den_pass_smem(F);
   if (F.nd <= 8) {
-    FCUDA(cudaFuncSetAttribute(den_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCUDA(raise_smem_attr(reinterpret_cast<const void*>(den_pass<8>), sm));
     den_pass<8><<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>(), src);
   } else {
-    FCUDA(cudaFuncSetAttribute(den_pass<kMaxCols>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCUDA(raise_smem_attr(reinterpret_cast<const void*>(den_pass<kMaxCols>), sm));
     den_pass<kMaxCols><<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton,
                                                      P->part.as<double>(), src);
   }
@@ -1816,14 +1842,13 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   FCUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned) * (n_groups + 1), s));
   FCUDA(fit_malloc((void**)&gpart.p, sizeof(double) * (size_t)n_groups * Wp));
   const size_t smstep = std::max(smk, den_pass_smem(F));
-  FCUDA(cudaFuncSetAttribute(min_step<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smstep));
-  FCUDA(cudaFuncSetAttribute(min_step<kMaxCols>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smstep));
+  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(min_step<8>), smstep));
+  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(min_step<kMaxCols>), smstep));
   // Constant-block factorization for the Schur-complement Newton solve.
   DevBuf prepb;
   FCUDA(fit_malloc((void**)&prepb.p, sizeof(double) * (size_t)prep_size(nn, nd)));
   const size_t smp = sizeof(double) * ((size_t)n * n + (size_t)nn * nn);
-  FCUDA(cudaFuncSetAttribute(min_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(min_prep), smp));
   min_prep<<<1, kFitThreads, smp, s>>>(R, S, nn, nd, prepb.as<double>());
   FCUDA(cudaGetLastError());
   const CtlSrc src{dctl, c.as<double>(), dc.as<double>(), S};
@@ -1888,7 +1913,7 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
   FCUDA(fit_malloc((void**)&gpart.p, sizeof(double) * (size_t)G * nd));
   FCUDA(fit_malloc((void**)&gsum.p, sizeof(double) * nd));
   const size_t smc = sizeof(double) * kMaxCols * kFitWarps + (size_t)kMaxCols * RPG_MAX_VARS + 16;
-  FCUDA(cudaFuncSetAttribute(den_colsum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc));
+  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(den_colsum), smc));
   den_colsum<<<G, kFitThreads, smc, s>>>(F, gpart.as<double>());
   sum_partials<<<1, 64, 0, s>>>(gpart.as<double>(), G, nd, gsum.as<double>());
   // start vector: least squares of the numerator basis against y
@@ -2079,7 +2104,7 @@ int fit_impl(const double* X, const double* dXs, const double* y, int64_t m, int
   FCUDA(fit_malloc((void**)&dscale.p, sizeof(double) * n));
   FCUDA(fit_malloc((void**)&dc.p, sizeof(double) * n));
   const size_t sm3 = sizeof(double) * (2 * (size_t)kMaxCols * kMaxCols + kMaxCols) + sizeof(int) * (kMaxCols + 4);
-  FCUDA(cudaFuncSetAttribute(svd_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
+  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(svd_small), sm3));
   svd_small<<<1, svd_threads(n), sm3, s>>>(dR.as<double>(), n, dsig.as<double>(), dV.as<double>(),
                                         dscale.as<double>(), nullptr, 1);
   FCUDA(cudaGetLastError());

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -563,8 +564,21 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     plan->threads = threads;
   }
   auto setup = [&](const void* fn, int* grid) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)plan->smem);
+    // Only ever raise a function's dynamic-SMEM limit (under a lock):
+    // plans of other models share the ahead-of-time kernels and may be
+    // created concurrently (rpg_plan_group_create) — lowering the limit
+    // under another plan's launch would fail it.
+    cudaError_t e;
+    {
+      static std::mutex mu;
+      static std::map<std::pair<const void*, int>, size_t> cur;
+      std::lock_guard<std::mutex> lk(mu);
+      size_t& c = cur[{fn, device}];
+      e = plan->smem <= c ? cudaSuccess
+                          : cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)plan->smem);
+      if (e == cudaSuccess && plan->smem > c) c = plan->smem;
+    }
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, plan->threads, plan->smem);
