@@ -492,6 +492,7 @@ struct MinCtl {
   double mu, phi0, decrement, alpha;  // alpha: first candidate of the next line pass
   double al[kAlphas];
   long long tail_cycles[2];           // RPG_FIT_TRACE: serial tail time (Newton, line)
+  long long newton_parts[3];          // ... of Newton steps: final fold, staging, solve
   int n_steps[2];
 };
 // Candidate source of a controlled den_pass: c, dc in equilibrated
@@ -1426,9 +1427,11 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
     R = Rs;
     if (prep && ph == kMinNewton) prep = Ps;
   }
+  const long long t_staged = clock64();
   if (ph == kMinNewton) {
     newton_body(R, S, gsum, pass_out, c, nn, nd, dc, ctl->mu, scratch, prep);
     __syncthreads();
+    if (threadIdx.x == 0) ctl->newton_parts[2] += clock64() - t_staged;
     if (threadIdx.x == 0) {
       if (!scratch->ok) {
         ctl->phase = kMinFail;  // non-finite KKT solution: empty result
@@ -1544,6 +1547,7 @@ min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __
   const int ph = ctl->phase;
   den_pass_reduce(gpart, n_groups, F.nd, pass_out);
   __syncthreads();
+  if (threadIdx.x == 0 && ph == kMinNewton) ctl->newton_parts[0] += clock64() - t0;
   ctl_step_body(R, S, gsum, pass_out, c, F.nn, F.nd, dc, ctl, scratch, prep);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1879,6 +1883,9 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
               hc.n_steps[0], hc.n_steps[1], hc.phase, hc.outer,
               hc.n_steps[0] ? hc.tail_cycles[0] / 1965.0 / hc.n_steps[0] : 0.0,
               hc.n_steps[1] ? hc.tail_cycles[1] / 1965.0 / hc.n_steps[1] : 0.0);
+    if (done && getenv("RPG_FIT_TRACE") && hc.n_steps[0])
+      fprintf(stderr, "[rpg_fit]   Newton tail: final fold %.1f us, solve %.1f us (rest: staging, control)\n",
+              hc.newton_parts[0] / 1965.0 / hc.n_steps[0], hc.newton_parts[2] / 1965.0 / hc.n_steps[0]);
   }
   if (hc.phase == kMinFail) return RPG_OK;
   to_raw<<<1, 32, 0, s>>>(c.as<double>(), S, n, out_raw, fin.as<int>());
