@@ -608,18 +608,34 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
   double gq = 0.0;  // thread t < nd owns sum (1/q) D[t]
   double gmma0 = 0.0, gmma1 = 0.0, gqv = 0.0;  // NDT == 8: DMMA accumulator fragment, column sums
   const int64_t nrow_tiles = (F.m + kPassRows - 1) / kPassRows;
+  // NDT == 8 with precomputed monomials: the next tile's row is loaded
+  // while the current one is processed (a CTA walks ~7 tiles; without the
+  // prefetch every tile exposes a full DRAM round trip).
+  double2 pre[4];
+  if (NDT == 8 && F.Dm) {
+    const int64_t r0 = (int64_t)blockIdx.x * kPassRows + threadIdx.x;
+    if (blockIdx.x < nrow_tiles && threadIdx.x < kPassRows && r0 < F.m) {
+      const double2* row = reinterpret_cast<const double2*>(F.Dm + r0 * 8);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) pre[k] = row[k];
+    }
+  }
   for (int64_t tile = blockIdx.x; tile < nrow_tiles; tile += gridDim.x) {
     const int64_t r = tile * kPassRows + threadIdx.x;
     const bool valid = threadIdx.x < kPassRows && r < F.m;
     double D[NDT];
     if (NDT == 8 && valid) {
       if (F.Dm) {
-        const double2* row = reinterpret_cast<const double2*>(F.Dm + r * 8);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const double2 v = row[k];
-          D[2 * k] = v.x;
-          D[2 * k + 1] = v.y;
+          D[2 * k] = pre[k].x;
+          D[2 * k + 1] = pre[k].y;
+        }
+        const int64_t rn = (tile + gridDim.x) * kPassRows + threadIdx.x;
+        if (tile + gridDim.x < nrow_tiles && rn < F.m) {
+          const double2* row = reinterpret_cast<const double2*>(F.Dm + rn * 8);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) pre[k] = row[k];
         }
       } else {
         double x[RPG_MAX_VARS];
@@ -1514,7 +1530,7 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
 constexpr int kStepGroup = 32;
 
 template <int NDT>
-__global__ void __launch_bounds__(kFitThreads, NDT == 8 ? 4 : 2)
+__global__ void __launch_bounds__(kFitThreads, NDT == 8 ? 3 : 2)
 min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __restrict__ pass_out,
          unsigned* __restrict__ counter /* n_groups + 1 */, double* __restrict__ gpart,
          const double* __restrict__ R, const double* __restrict__ S,
@@ -1781,7 +1797,7 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
     // reduction of the fused minimizer step).
     static const int per_sm = [] {
       const char* e = getenv("RPG_FIT_PASS_CTAS");
-      return e ? std::max(1, atoi(e)) : 4;
+      return e ? std::max(1, atoi(e)) : 3;  // min_step<8>'s launch bounds
     }();
     P->G = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)per_sm * sms));
     P->nd = F.nd;
