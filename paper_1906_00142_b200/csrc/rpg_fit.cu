@@ -115,12 +115,17 @@ __device__ void fold_tile(double* R, double* T, int rows, int ld, int n, double*
 }
 
 // eval_monomial (polyfit.hpp:96-105) for one sample and exponent row.
-__device__ __forceinline__ double monomial(const double* x, const uint8_t* e, int nv) {
+__device__ __forceinline__ double monomial(const double (&x)[RPG_MAX_VARS], const uint8_t* e, int nv) {
+  // Unrolled over the variables so x stays in registers (a runtime index
+  // would put it in local memory); the product order is eval_monomial's.
   double m = 1.0;
-  for (int v = 0; v < nv; ++v) {
-    double p = 1.0;
-    for (int t = 0; t < e[v]; ++t) p *= x[v];
-    m *= p;
+#pragma unroll
+  for (int v = 0; v < RPG_MAX_VARS; ++v) {
+    if (v < nv) {
+      double p = 1.0;
+      for (int t = 0; t < e[v]; ++t) p *= x[v];
+      m *= p;
+    }
   }
   return m;
 }
