@@ -1832,6 +1832,7 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
               char* err, size_t errlen) {
   const int nn = F.nn, nd = F.nd, n = F.n;
   *found = 0;
+  const auto t_begin = std::chrono::steady_clock::now();
   DevBuf c, dc, cd, st, fin;
   FCUDA(fit_malloc((void**)&c.p, sizeof(double) * n));
   FCUDA(fit_malloc((void**)&dc.p, sizeof(double) * n));
@@ -1897,6 +1898,11 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
     FCUDA(cudaMemcpyAsync(&hc, ctlb.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     FCUDA(cudaStreamSynchronize(s));
     done = hc.phase >= kMinDone;
+    if (done && getenv("RPG_FIT_TRACE"))
+      fprintf(stderr, "[rpg_fit] minimizer wall %.3f ms = %.1f us per step\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count(),
+              1e3 * std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count() /
+                  std::max(1, hc.n_steps[0] + hc.n_steps[1]));
     if (done && getenv("RPG_FIT_TRACE"))
       fprintf(stderr,
               "[rpg_fit] minimizer: %d Newton + %d line steps, phase %d, outer %d; serial tail "
