@@ -1101,15 +1101,30 @@ __device__ void newton_schur_fast(const double* R, const double* __restrict__ S,
   double* tu = ws + 128;      // 64
   double* rhs = ws + 192;     // 16
   double* xs = ws + 208;      // 16
+  double* cv = ws + 224;      // 64: S .* c
+  // One round of global loads for every small input the solve reads more
+  // than once (S, the pass sums, gsum); c only for cv.
+  double* Ss = ws + 288;      // 64
+  double* po = ws + 352;      // <= 2 kAlphas + 8 + 64 = 80
+  double* gs = ws + 432;      // 8
+  const int W = 2 * kAlphas + nd + nd * nd;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const double sk = S[k];
+    Ss[k] = sk;
+    cv[k] = sk * c[k];
+  }
+  for (int e = threadIdx.x; e < W; e += blockDim.x) po[e] = pass_out[e];
+  for (int e = threadIdx.x; e < nd; e += blockDim.x) gs[e] = gsum[e];
+  __syncthreads();
+  S = Ss;
+  pass_out = po;
+  gsum = gs;
   const double* gq = pass_out + 2 * kAlphas;
   const double* G = gq + nd;
   const double* Ainv = P + 1;
   const double* B = Ainv + nn * nn;
   const double* Fm = B + nn * nd;
   const double* Sv0 = Fm + nn * nd;
-  double* cv = ws + 224;      // 64: S .* c
-  for (int k = threadIdx.x; k < n; k += blockDim.x) cv[k] = S[k] * c[k];
-  __syncthreads();
   r_rows(R, cv, n, RSc, 0);
   __syncthreads();
   for (int k = warp; k < n; k += nw) {
@@ -1163,19 +1178,21 @@ __device__ void newton_schur_fast(const double* R, const double* __restrict__ S,
     if (lane == 0) st->ok = sing ? 0 : 1;
   }
   __syncthreads();
+  double* dcs = ws + 440;     // 64: dc, also kept here for the decrement
   for (int i = threadIdx.x; i < nn; i += blockDim.x) {
     double t = tu[i];
     for (int j = 0; j < nd; ++j) t -= Fm[i * nd + j] * xs[j];
     dc[i] = t;
+    dcs[i] = t;
   }
-  for (int j = threadIdx.x; j < nd; j += blockDim.x) dc[nn + j] = xs[j];
+  for (int j = threadIdx.x; j < nd; j += blockDim.x) dc[nn + j] = dcs[nn + j] = xs[j];
   __syncthreads();
   if (warp == 0) {
     double d = 0.0;
     bool fin = true;
     for (int k = lane; k < n; k += 32) {
-      fin &= isfinite(dc[k]);
-      d = fma(-grad[k], dc[k], d);
+      fin &= isfinite(dcs[k]);
+      d = fma(-grad[k], dcs[k], d);
     }
     d = warp_sum(d);
     fin = __all_sync(0xffffffffu, fin);
