@@ -141,7 +141,8 @@ __device__ void build_tile(const FitParams& F, int64_t r0, double* T, const uint
       continue;
     }
     double x[RPG_MAX_VARS];
-    for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
+#pragma unroll
+    for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
     const double yv = F.y[r];
     const double wr = F.w ? F.w[r] : 1.0;
     for (int k = 0; k < F.nn; ++k) {
@@ -344,7 +345,8 @@ __global__ void den_stats(const FitParams F, const double* __restrict__ cden,
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < F.m;
        r += (int64_t)gridDim.x * blockDim.x) {
     double x[RPG_MAX_VARS];
-    for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
+#pragma unroll
+    for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
     double q = 0.0;
     for (int k = 0; k < F.nd; ++k) q = fma(monomial(x, sexps + k * F.n_vars, F.n_vars), cden[k], q);
     qmin = fmin(qmin, q);
@@ -464,7 +466,8 @@ __global__ void den_colsum(const FitParams F, double* __restrict__ partial) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < F.m;
        r += (int64_t)gridDim.x * blockDim.x) {
     double x[RPG_MAX_VARS];
-    for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
+#pragma unroll
+    for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
     for (int k = 0; k < F.nd; ++k) loc[k] += monomial(x, sexps + k * F.n_vars, F.n_vars);
   }
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -530,7 +533,8 @@ __global__ void den_monomials(const FitParams F, double* __restrict__ Dm) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < F.m;
        r += (int64_t)gridDim.x * blockDim.x) {
     double x[RPG_MAX_VARS];
-    for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
+#pragma unroll
+    for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
     const int st = F.nd <= 8 ? 8 : F.nd;  // stride 8 (zero-padded) for den_pass<8>
     for (int k = 0; k < st; ++k)
       Dm[r * st + k] = k < F.nd ? monomial(x, F.exps + (size_t)(F.nn + k) * F.n_vars, F.n_vars) : 0.0;
@@ -1617,7 +1621,8 @@ __global__ void row_weights(const FitParams F, const double* __restrict__ cd,
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < F.m;
        r += (int64_t)gridDim.x * blockDim.x) {
     double x[RPG_MAX_VARS];
-    for (int v = 0; v < F.n_vars; ++v) x[v] = F.X[r * F.n_vars + v];
+#pragma unroll
+    for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
     double q = 0.0;
     for (int k = 0; k < F.nd; ++k) q = fma(monomial(x, sexps + k * F.n_vars, F.n_vars), cd[k], q);
     w[r] = fmax(1.0, fabs(F.y[r])) * q;
