@@ -145,6 +145,22 @@ static void ir_tests() {
   CHECK(throws_with<ir::ParseError>([] { ir::parse("inputs: a\noutput: y\n0: add y a 1.5\n"); },
                                     "decimal literals"));
   CHECK(throws_with<ir::ParseError>([] { ir::parse("inputs: a\noutput: y\n"); }, "empty program body"));
+  // make_binding_plan's errors (pipeline.hpp:482-516) surface before any GPU
+  // work: an unknown input, a data parameter the tuple does not have.
+  perf::DeviceProfile hw = perf::parse_profile(
+      "R_max = 65536\nZ_max = 12288\nT_max = 1024\nB_max = 8\nW_max = 48\nnum_SM = 16\n"
+      "freq_GHz = 1.3\nmem_latency_cycles = 436\ndeparture_del_coal_cycles = 4\n"
+      "departure_del_uncoal_cycles = 40\nmem_bandwidth_GBps = 144\nissue_cycles = 4\n"
+      "load_bytes_per_warp = 128\nuncoal_per_mw = 32\n");
+  const auto space = data::enumerate_configs();
+  ir::RationalProgram q7 = ir::parse("inputs: Q7 bx\noutput: y\n0: mul y Q7 bx\n1: halt_return y\n");
+  CHECK(throws_with<pipe::PipelineError>([&] { pipe::search_optimal(q7, {64}, hw, space); },
+                                         "program input 'Q7' is neither a block dimension"));
+  ir::RationalProgram d2 = ir::parse("inputs: D2 bx\noutput: y\n0: mul y D2 bx\n1: halt_return y\n");
+  CHECK(throws_with<pipe::PipelineError>([&] { pipe::search_optimal(d2, {64}, hw, space); },
+                                         "program input 'D2' has no value: 1 data parameter(s) were given"));
+  CHECK(throws_with<std::invalid_argument>([&] { pipe::search_optimal(d2, {64, 3}, hw, {}); },
+                                           "configuration space is empty"));
 }
 
 static rpg_profile prof(const perf::DeviceProfile& hw) { return pipe::detail::to_rpg(hw); }
