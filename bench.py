@@ -138,8 +138,8 @@ def official_flops(spec) -> int:
 def default_arith(workload: str, kernel: str) -> str:
     """The arithmetic mode a workload is benchmarked in: the configuration-
     major FAST_CM search for the one-data-parameter C2/C3/C6 models (specialized
-    kernels only), FAST otherwise (C5's two data parameters, the Ec dump)."""
-    return "fastcm" if workload in ("c2", "c3", "c6") and kernel == "specialized" else "fast"
+    kernels only; also the Ec dump), FAST otherwise (C5's two data parameters)."""
+    return "fastcm" if workload in ("c2", "c3", "c6", "dump") and kernel == "specialized" else "fast"
 
 
 def count_kernel_launches(fn, prefix="rpg_"):

@@ -78,7 +78,7 @@ def test_default_arith_per_workload():
     assert bench.default_arith("c2", "specialized") == "fastcm"
     assert bench.default_arith("c3", "specialized") == "fastcm"
     assert bench.default_arith("c5", "specialized") == "fast"
-    assert bench.default_arith("dump", "specialized") == "fast"
+    assert bench.default_arith("dump", "specialized") == "fastcm"
     assert bench.default_arith("c2", "generic") == "fast"
 
 
