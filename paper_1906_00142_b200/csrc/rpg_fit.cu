@@ -1725,6 +1725,15 @@ cudaError_t fit_malloc(void** p, size_t bytes) {
   return g_fit_stream ? cudaMallocAsync(p, bytes, g_fit_stream) : cudaMalloc(p, bytes);
 }
 
+// RPG_FIT_NO_DMMA=1: the sample passes of nd <= 8 denominators use the
+// generic kernels (Gram of D/q with FMA chains) instead of the
+// register-resident nd = 8 path with the FP64 tensor-core Gram
+// (mma.m8n8k4.f64) — the A/B switch behind DESIGN.md's DMMA measurement.
+inline bool fit_use_dmma() {
+  static const bool on = getenv("RPG_FIT_NO_DMMA") == nullptr;
+  return on;
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only ever raised, under a
 // lock: concurrent fits (rpg_fit_rational_multi) with different column
 // counts must not lower the limit under another thread's launch.
@@ -1832,7 +1841,7 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
     FCUDA(fit_malloc((void**)&P->out.p, sizeof(double) * W));
   }
   const size_t sm = den_pass_smem(F);
-  if (F.nd <= 8) {
+  if (F.nd <= 8 && fit_use_dmma()) {
     FCUDA(raise_smem_attr(reinterpret_cast<const void*>(den_pass<8>), sm));
     den_pass<8><<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>(), src);
   } else {
@@ -1906,7 +1915,7 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   constexpr int kChunk = 24;
   for (int done = 0, steps = 0; !done && steps < 16 * 40 * 16; steps += kChunk) {
     for (int i = 0; i < kChunk; ++i) {
-      if (F.nd <= 8)
+      if (F.nd <= 8 && fit_use_dmma())
         min_step<8><<<P.G, kFitThreads, smstep, s>>>(F, src, P.part.as<double>(), P.out.as<double>(),
                                                      counter.as<unsigned>(), gpart.as<double>(), R, S,
                                                      gsum, c.as<double>(), dc.as<double>(), dctl,
