@@ -1556,7 +1556,7 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
 constexpr int kStepGroup = 32;
 
 template <int NDT>
-__global__ void __launch_bounds__(kFitThreads, NDT == 8 ? 3 : 2)
+__global__ void __launch_bounds__(kFitThreads, 2)
 min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __restrict__ pass_out,
          unsigned* __restrict__ counter /* n_groups + 1 */, double* __restrict__ gpart,
          const double* __restrict__ R, const double* __restrict__ S,
@@ -1833,7 +1833,7 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
     // reduction of the fused minimizer step).
     static const int per_sm = [] {
       const char* e = getenv("RPG_FIT_PASS_CTAS");
-      return e ? std::max(1, atoi(e)) : 3;  // min_step<8>'s launch bounds
+      return e ? std::max(1, atoi(e)) : 2;  // min_step's launch bounds (r02k: 47 vs 51 ms at 3)
     }();
     P->G = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)per_sm * sms));
     P->nd = F.nd;
