@@ -60,6 +60,8 @@ struct FitParams {
   int32_t with_y_col;           // 1: append y as column n (TSQR of [V | y])
   int32_t num_only;             // 1: numerator block only (start-vector LS)
   const double* Dm;             // optional m x nd raw denominator monomials (den_pass)
+  int32_t den01;                // 1: n_vars <= 4 and every denominator exponent <= 1
+  int32_t den_lat3;             // 1: 3 variables, denominator basis = monomial_basis({1,1,1})
 };
 
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
@@ -502,7 +504,17 @@ struct MinCtl {
   long long tail_cycles[2];           // RPG_FIT_TRACE: serial tail time (Newton, line)
   long long newton_parts[3];          // ... of Newton steps: final fold, staging, solve
   int n_steps[2];
+  // %globaltimer ns: CTA 0's start of the current step, end of the previous
+  // step; summed sample-pass span (start -> last CTA's arrival) and
+  // inter-step gap (previous end -> start).
+  unsigned long long t_start, t_prev_end, pass_ns, gap_ns, tail_ns, t_arrive;
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 // Candidate source of a controlled den_pass: c, dc in equilibrated
 // coordinates, S the column scale.
 struct CtlSrc {
@@ -525,6 +537,12 @@ __device__ __forceinline__ double split_mant(double q, int& e) {
   const double m = frexp(q, &e2);
   e += e2;
   return m;
+}
+
+// |v| in [2^-500, 2^500) (biased exponent in [523, 1523)): products of two
+// such numbers are normal.
+__device__ __forceinline__ bool mid_range(double v) {
+  return (unsigned)(((__double2hiint(v) >> 20) & 0x7ff) - 523) < 1000u;
 }
 
 // Raw denominator monomials of every sample (m x nd), computed once per fit
@@ -621,6 +639,31 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
   // while the current one is processed (a CTA walks ~7 tiles; without the
   // prefetch every tile exposes a full DRAM round trip).
   double2 pre[4];
+  // den01 without Dm: the monomials are recomputed from x by bit masks
+  // (4 bits per monomial, bit v = exponent 1 on variable v), x of the next
+  // tile prefetched into pre[0..1].
+  const bool x01 = NDT == 8 && !F.Dm && F.den01;
+  uint32_t dm4 = 0;
+  bool lattice3 = false;
+  if (x01) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (k < nd && v < F.n_vars && sexps[k * F.n_vars + v]) dm4 |= 1u << (4 * k + v);
+    // monomial_basis({1, 1, 1}) (polyfit.hpp:50-73): 1, x2, x1, x0, x1x2,
+    // x0x2, x0x1, x0x1x2 — bit v of each nibble = exponent of x_v
+    lattice3 = nd == 8 && F.n_vars == 3 && dm4 == 0x73561240u;
+    const int64_t r0 = (int64_t)blockIdx.x * kPassRows + threadIdx.x;
+    pre[0] = pre[1] = make_double2(0.0, 0.0);
+    if (blockIdx.x < nrow_tiles && threadIdx.x < kPassRows && r0 < F.m) {
+      const double* xr = F.X + r0 * F.n_vars;
+      pre[0].x = xr[0];
+      if (F.n_vars > 1) pre[0].y = xr[1];
+      if (F.n_vars > 2) pre[1].x = xr[2];
+      if (F.n_vars > 3) pre[1].y = xr[3];
+    }
+  }
   if (NDT == 8 && F.Dm) {
     const int64_t r0 = (int64_t)blockIdx.x * kPassRows + threadIdx.x;
     if (blockIdx.x < nrow_tiles && threadIdx.x < kPassRows && r0 < F.m) {
@@ -646,6 +689,41 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
 #pragma unroll
           for (int k = 0; k < 4; ++k) pre[k] = row[k];
         }
+      } else if (x01) {
+        // monomial()'s product order with the exponent-0 factors (exact
+        // multiplications by 1) skipped.
+        const double x[4] = {pre[0].x, pre[0].y, pre[1].x, pre[1].y};
+        if (lattice3) {
+          // the full {0,1}^3 basis in monomial_basis order: every product
+          // extends a shorter one by its highest variable, as monomial()
+          // multiplies (((1 x0) x1) x2) — 4 multiplies per row
+          const double p01 = x[0] * x[1], p02 = x[0] * x[2], p12 = x[1] * x[2];
+          D[0] = 1.0;
+          D[1] = x[2];
+          D[2] = x[1];
+          D[3] = x[0];
+          D[4] = p12;
+          D[5] = p02;
+          D[6] = p01;
+          D[7] = p01 * x[2];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            double mo = 1.0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              if ((dm4 >> (4 * k + v)) & 1u) mo *= x[v];
+            D[k] = k < nd ? mo : 0.0;
+          }
+        }
+        const int64_t rn = (tile + gridDim.x) * kPassRows + threadIdx.x;
+        if (tile + gridDim.x < nrow_tiles && rn < F.m) {
+          const double* xr = F.X + rn * F.n_vars;
+          pre[0].x = xr[0];
+          if (F.n_vars > 1) pre[0].y = xr[1];
+          if (F.n_vars > 2) pre[1].x = xr[2];
+          if (F.n_vars > 3) pre[1].y = xr[3];
+        }
       } else {
         double x[RPG_MAX_VARS];
 #pragma unroll
@@ -665,7 +743,12 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
         if (a < n_alpha) {
           const double q = has_dir ? fma(al[a], qd, q0) : q0;
           qmin[a] = fmin(qmin[a], q);
-          prod[a] *= split_mant(q, pexp[a]);
+          // mid-range q multiplies in unsplit: prod stays a power-of-two
+          // multiple of the normalized product and every multiply rounds
+          // on normal numbers, so the mantissa / exponent sums are those
+          // of splitting every factor
+          if (mid_range(q)) prod[a] *= q;
+          else prod[a] *= split_mant(q, pexp[a]);
         }
       }
     } else if (valid) {
@@ -699,7 +782,8 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
       }
     }
 #pragma unroll
-    for (int a = 0; a < kAlphas; ++a) prod[a] = split_mant(prod[a], pexp[a]);  // keep products in range
+    for (int a = 0; a < kAlphas; ++a)  // keep products in range
+      if (NDT != 8 || !mid_range(prod[a])) prod[a] = split_mant(prod[a], pexp[a]);
     if (newton) {
       __syncthreads();
       if (threadIdx.x < kPassRows) {
@@ -797,7 +881,12 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
     }
   }
 #pragma unroll
-  for (int a = 0; a < kAlphas; ++a) slog[a] = fma((double)pexp[a], 0.69314718055994530942, log(prod[a]));
+  for (int a = 0; a < kAlphas; ++a) {
+    // normalized as after the per-tile split of every tile (CTAs past the
+    // last tile never split: prod 1, exponent 0)
+    if (NDT == 8 && (int64_t)blockIdx.x < nrow_tiles) prod[a] = split_mant(prod[a], pexp[a]);
+    slog[a] = fma((double)pexp[a], 0.69314718055994530942, log(prod[a]));
+  }
   double* out = partial + (size_t)blockIdx.x * (2 * kAlphas + nd + nd * nd);
 #pragma unroll
   for (int a = 0; a < kAlphas; ++a) {
@@ -837,13 +926,299 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// The nd <= 8 sample pass (FP64 tensor-core Gram), specialized by where a
+// row's denominator monomials come from (den_src):
+//   kSrcDm      the precomputed m x 8 array (den_monomials),
+//   kSrcLat3    x of 3 variables, denominator basis = monomial_basis({1,1,1})
+//               (polyfit.hpp:50-73): 4 multiplies per row,
+//   kSrcMask    x of <= 4 variables, 0/1 exponents: bit-mask products,
+//   kSrcGeneric x, any exponents: monomial().
+// Every source yields monomial()'s bits, so all four give identical sums.
+// The row loop is straight-line: the next tile's row is prefetched into the
+// row buffer while the current one is consumed, rows past m read row m-1
+// and contribute nothing (q -> +inf for the minimum, 1 for the product, 0
+// for the Gram).
+enum { kSrcDm = 0, kSrcLat3 = 1, kSrcMask = 2, kSrcGeneric = 3 };
+
+template <int SRC>
+struct Row8 {
+  double v[SRC == kSrcLat3 ? 3 : SRC == kSrcMask ? 4 : 8];
+};
+
+template <int SRC>
+__device__ __forceinline__ void load_row8(const FitParams& F, int64_t r, Row8<SRC>& b) {
+  if constexpr (SRC == kSrcDm) {
+    const double2* p = reinterpret_cast<const double2*>(F.Dm + r * 8);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 t = __ldg(p + k);
+      b.v[2 * k] = t.x;
+      b.v[2 * k + 1] = t.y;
+    }
+  } else if constexpr (SRC == kSrcLat3) {
+    const double* p = F.X + r * 3;
+#pragma unroll
+    for (int v = 0; v < 3; ++v) b.v[v] = __ldg(p + v);
+  } else {
+    const int nv = F.n_vars;
+    const double* p = F.X + r * nv;
+    constexpr int kV = SRC == kSrcMask ? 4 : RPG_MAX_VARS;
+#pragma unroll
+    for (int v = 0; v < kV; ++v) b.v[v] = v < nv ? __ldg(p + v) : 0.0;
+  }
+}
+
+template <int SRC>
+__device__ __forceinline__ void row_monomials8(const FitParams& F, const Row8<SRC>& b, uint32_t dm4,
+                                               const uint8_t* sexps, double (&D)[8]) {
+  const int nd = F.nd;
+  if constexpr (SRC == kSrcDm) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) D[k] = b.v[k];  // zero-padded past nd
+  } else if constexpr (SRC == kSrcLat3) {
+    // 1, x2, x1, x0, x1x2, x0x2, x0x1, x0x1x2: each product extends a
+    // shorter one by its highest variable, as monomial() multiplies
+    const double p01 = b.v[0] * b.v[1], p02 = b.v[0] * b.v[2], p12 = b.v[1] * b.v[2];
+    D[0] = 1.0;
+    D[1] = b.v[2];
+    D[2] = b.v[1];
+    D[3] = b.v[0];
+    D[4] = p12;
+    D[5] = p02;
+    D[6] = p01;
+    D[7] = p01 * b.v[2];
+  } else if constexpr (SRC == kSrcMask) {
+    // monomial()'s order with the exponent-0 factors (exact multiplies by
+    // 1) skipped
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double mo = 1.0;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if ((dm4 >> (4 * k + v)) & 1u) mo *= b.v[v];
+      D[k] = k < nd ? mo : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) D[k] = k < nd ? monomial(b.v, sexps + k * F.n_vars, F.n_vars) : 0.0;
+  }
+}
+
+// One row's contribution to candidate a: min q and the log-sum's mantissa
+// product / exponent (mid-range factors multiply in unsplit; see
+// mid_range).  Rows past m pass q = +inf / 1.
+__device__ __forceinline__ void accum_q(double q, bool valid, double& qmin, double& prod, int& pexp) {
+  qmin = fmin(qmin, valid ? q : INFINITY);
+  const double qp = valid ? q : 1.0;
+  if (mid_range(qp)) prod *= qp;
+  else prod *= split_mant(qp, pexp);
+}
+
+template <int SRC, bool DIR>
+__device__ __forceinline__ void rows8(const FitParams& F, int64_t nrow_tiles, const double* cands,
+                                      const double (&al)[kAlphas], int n_alpha, bool newton,
+                                      uint32_t dm4, const uint8_t* sexps, double (&qmin)[kAlphas],
+                                      double (&prod)[kAlphas], int (&pexp)[kAlphas], double* U,
+                                      double& gmma0, double& gmma1, double& gqv) {
+  const int nd = F.nd;
+  const int64_t step = (int64_t)gridDim.x * kPassRows, last = F.m - 1;
+  int64_t r = (int64_t)blockIdx.x * kPassRows + threadIdx.x;
+  Row8<SRC> buf;
+  if ((int64_t)blockIdx.x < nrow_tiles) load_row8<SRC>(F, r < last ? r : last, buf);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t tile = blockIdx.x; tile < nrow_tiles; tile += gridDim.x, r += step) {
+    const bool valid = r < F.m;
+    double D[8];
+    row_monomials8<SRC>(F, buf, dm4, sexps, D);
+    if (tile + gridDim.x < nrow_tiles) {
+      const int64_t rn = r + step;
+      load_row8<SRC>(F, rn < last ? rn : last, buf);
+    }
+    double q0 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q0 = fma(D[k], cands[k], q0);
+    if constexpr (DIR) {
+      // q_a = D.(cd + al_a dd) evaluated as D.cd + al_a (D.dd)
+      double qd = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) qd = fma(D[k], cands[8 + k], qd);
+#pragma unroll
+      for (int a = 0; a < kAlphas; ++a)
+        if (a < n_alpha) accum_q(fma(al[a], qd, q0), valid, qmin[a], prod[a], pexp[a]);
+    } else {
+#pragma unroll
+      for (int a = 0; a < kAlphas; ++a)
+        if (a < n_alpha) accum_q(q0, valid, qmin[a], prod[a], pexp[a]);
+      if (newton) {
+        // U = D / q for the Gram U^T U and the column sums, on the FP64
+        // tensor cores: warp w folds rows [32w, 32w + 32) in 4-row chunks
+        // with mma.m8n8k4 (A = U^T chunk, B = U chunk: lane l supplies
+        // U[r0 + l%4][l/4] to both).
+        const double qi = 1.0 / q0;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) U[threadIdx.x * 8 + k] = (valid && k < nd) ? D[k] * qi : 0.0;
+        __syncthreads();
+#pragma unroll
+        for (int cidx = 0; cidx < 8; ++cidx) {
+          const double v = U[(warp * 32 + cidx * 4 + (lane & 3)) * 8 + (lane >> 2)];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(gmma0), "+d"(gmma1) : "d"(v), "d"(v));
+          gqv += v;
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < kAlphas; ++a)  // keep the products in range
+      if (!mid_range(prod[a])) prod[a] = split_mant(prod[a], pexp[a]);
+  }
+}
+
+// Per-candidate min q and sum log q of the CTA's rows into out[2a], out[2a+1]
+// (warp shuffles, then warps 0..7 in order; buf: >= 2 kAlphas kFitWarps
+// doubles of SMEM free after the leading barrier).
+__device__ __forceinline__ void write_alpha_partials(const double (&qmin)[kAlphas],
+                                                     const double (&slog)[kAlphas], double* buf,
+                                                     double* out) {
+  double t[kAlphas], u[kAlphas];
+#pragma unroll
+  for (int a = 0; a < kAlphas; ++a) {
+    t[a] = qmin[a];
+    u[a] = slog[a];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int a = 0; a < kAlphas; ++a) {
+      t[a] = fmin(t[a], __shfl_xor_sync(0xffffffffu, t[a], o));
+      u[a] += __shfl_xor_sync(0xffffffffu, u[a], o);
+    }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < kAlphas; ++a) {
+      buf[a * 2 * kFitWarps + (threadIdx.x >> 5)] = t[a];
+      buf[a * 2 * kFitWarps + kFitWarps + (threadIdx.x >> 5)] = u[a];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kAlphas) {
+    const double* b = buf + threadIdx.x * 2 * kFitWarps;
+    double mn = b[0], sm = b[kFitWarps];
+    for (int i = 1; i < kFitWarps; ++i) {
+      mn = fmin(mn, b[i]);
+      sm += b[kFitWarps + i];
+    }
+    out[2 * threadIdx.x] = mn;
+    out[2 * threadIdx.x + 1] = sm;
+  }
+}
+
+template <int SRC>
+__device__ __forceinline__ void den_pass8_body(const FitParams& F, const double* __restrict__ cd,
+                                               const double* __restrict__ dd,
+                                               const double* __restrict__ alphas, int n_alpha,
+                                               int newton, double* __restrict__ partial,
+                                               const CtlSrc& src) {
+  extern __shared__ __align__(16) double fsm[];
+  const int nd = F.nd;
+  if (src.ctl) {
+    // Controlled pass: NEWTON = candidate S.*c (with the Newton sums), LINE =
+    // S.*c + al[a] (S.*dc) for the pass's candidates; nothing once finished.
+    const int ph = src.ctl->phase;
+    if (ph >= kMinDone) return;
+    newton = ph == kMinNewton;
+    n_alpha = newton ? 1 : src.ctl->n_alpha;
+  }
+  double* U = fsm;                        // kPassRows x 8 (row-major, zero-padded)
+  double* cands = U + kPassRows * 8 + 32;  // cd[8], dd[8] (den_pass_smem's layout)
+  uint8_t* sexps = reinterpret_cast<uint8_t*>(cands + kAlphas * (nd > 4 ? nd : 4));
+  if constexpr (SRC == kSrcMask || SRC == kSrcGeneric)
+    for (int e = threadIdx.x; e < nd * F.n_vars; e += blockDim.x) sexps[e] = F.exps[F.nn * F.n_vars + e];
+  const bool has_dir = src.ctl ? !newton : dd != nullptr;
+  double al[kAlphas];
+#pragma unroll
+  for (int a = 0; a < kAlphas; ++a)
+    al[a] = a < n_alpha ? (src.ctl ? src.ctl->al[a] : (alphas ? alphas[a] : 0.0)) : 0.0;
+  if (threadIdx.x < 16) {
+    const int k = threadIdx.x & 7;
+    double v = 0.0;
+    if (k < nd) {
+      if (threadIdx.x < 8) v = src.ctl ? src.S[F.nn + k] * src.c[F.nn + k] : cd[k];
+      else if (has_dir) v = src.ctl ? src.S[F.nn + k] * src.dc[F.nn + k] : dd[k];
+    }
+    cands[threadIdx.x] = v;
+  }
+  __syncthreads();
+  uint32_t dm4 = 0;
+  if constexpr (SRC == kSrcMask) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (k < nd && v < F.n_vars && sexps[k * F.n_vars + v]) dm4 |= 1u << (4 * k + v);
+  }
+  double qmin[kAlphas], prod[kAlphas], slog[kAlphas];
+  int pexp[kAlphas];
+#pragma unroll
+  for (int a = 0; a < kAlphas; ++a) {
+    qmin[a] = INFINITY;
+    prod[a] = 1.0;
+    pexp[a] = 0;
+  }
+  double gmma0 = 0.0, gmma1 = 0.0, gqv = 0.0;  // DMMA accumulator fragment, column sums
+  const int64_t nrow_tiles = (F.m + kPassRows - 1) / kPassRows;
+  if (has_dir)
+    rows8<SRC, true>(F, nrow_tiles, cands, al, n_alpha, false, dm4, sexps, qmin, prod, pexp, U, gmma0,
+                     gmma1, gqv);
+  else
+    rows8<SRC, false>(F, nrow_tiles, cands, al, n_alpha, newton, dm4, sexps, qmin, prod, pexp, U, gmma0,
+                      gmma1, gqv);
+  double* out = partial + (size_t)blockIdx.x * (2 * kAlphas + nd + nd * nd);
+  double gram = 0.0, gq = 0.0;
+  if (newton) {
+    // Fold the 8 warps' fragments (fixed order): thread t holds
+    // G[t/4][2(t%4) + {0,1}] of its warp; column sums by column t/4.
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    gqv += __shfl_xor_sync(0xffffffffu, gqv, 1);
+    gqv += __shfl_xor_sync(0xffffffffu, gqv, 2);
+    __syncthreads();
+    double* Pm = U;  // 8 warps x (64 Gram + 8 column sums)
+    Pm[warp * 72 + (lane >> 2) * 8 + 2 * (lane & 3)] = gmma0;
+    Pm[warp * 72 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = gmma1;
+    if ((lane & 3) == 0) Pm[warp * 72 + 64 + (lane >> 2)] = gqv;
+    __syncthreads();
+    if (threadIdx.x < 72) {
+      double t = 0.0;
+      for (int w = 0; w < kFitWarps; ++w) t += Pm[w * 72 + threadIdx.x];
+      if (threadIdx.x < 64) gram = t;
+      else gq = t;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < kAlphas; ++a) {
+    // normalized as after the per-tile split of every tile (CTAs past the
+    // last tile never split: prod 1, exponent 0)
+    if ((int64_t)blockIdx.x < nrow_tiles) prod[a] = split_mant(prod[a], pexp[a]);
+    slog[a] = fma((double)pexp[a], 0.69314718055994530942, log(prod[a]));
+  }
+  write_alpha_partials(qmin, slog, U + 72 * kFitWarps, out);
+  if (newton) {
+    const int t = threadIdx.x;
+    if (t < 64 && (t >> 3) < nd && (t & 7) < nd) out[2 * kAlphas + nd + (t >> 3) * nd + (t & 7)] = gram;
+    if (t >= 64 && t < 64 + nd) out[2 * kAlphas + (t - 64)] = gq;
+  }
+}
+
 // Sums the per-block partials of den_pass (min for the q minima).
-template <int NDT>
+template <int NDT, int SRC = kSrcDm>
 __global__ void __launch_bounds__(kFitThreads)
 den_pass(const FitParams F, const double* __restrict__ cd, const double* __restrict__ dd,
          const double* __restrict__ alphas, int n_alpha, int newton,
          double* __restrict__ partial /* per block: 2*kAlphas + nd + nd*nd */, CtlSrc src) {
-  den_pass_body<NDT>(F, cd, dd, alphas, n_alpha, newton, partial, src);
+  if constexpr (NDT == 8) den_pass8_body<SRC>(F, cd, dd, alphas, n_alpha, newton, partial, src);
+  else den_pass_body<NDT>(F, cd, dd, alphas, n_alpha, newton, partial, src);
 }
 
 // Folds G per-block partials (W values each) into out: one thread per
@@ -1555,15 +1930,23 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
 // arrives last.  No-op for every CTA once the loop is done.
 constexpr int kStepGroup = 32;
 
-template <int NDT>
+template <int NDT, int SRC = kSrcDm>
 __global__ void __launch_bounds__(kFitThreads, 2)
 min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __restrict__ pass_out,
          unsigned* __restrict__ counter /* n_groups + 1 */, double* __restrict__ gpart,
          const double* __restrict__ R, const double* __restrict__ S,
          const double* __restrict__ gsum, double* __restrict__ c, double* __restrict__ dc,
          MinCtl* __restrict__ ctl, MinState* __restrict__ scratch, const double* __restrict__ prep) {
+  // Programmatic dependent launch (fit_use_pdl): let the next step's grid
+  // launch now — its CTAs take the SM slots this grid's CTAs free and wait
+  // below — then wait for the previous step's grid to complete (its memory
+  // visible).  Both are no-ops without the launch attribute.
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (src.ctl->phase >= kMinDone) return;
-  den_pass_body<NDT>(F, nullptr, nullptr, nullptr, 1, 1, partial, src);
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_start = global_ns();
+  if constexpr (NDT == 8) den_pass8_body<SRC>(F, nullptr, nullptr, nullptr, 1, 1, partial, src);
+  else den_pass_body<NDT>(F, nullptr, nullptr, nullptr, 1, 1, partial, src);
   const int W = 2 * kAlphas + F.nd + F.nd * F.nd;
   const int G = gridDim.x, n_groups = (G + kStepGroup - 1) / kStepGroup;
   const int group = blockIdx.x / kStepGroup;
@@ -1587,6 +1970,12 @@ min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __
   __threadfence();
   const long long t0 = clock64();
   const int ph = ctl->phase;
+  if (threadIdx.x == 0) {
+    const unsigned long long ts = ctl->t_start;
+    ctl->t_arrive = global_ns();
+    ctl->pass_ns += ctl->t_arrive - ts;
+    if (ctl->t_prev_end) ctl->gap_ns += ts - ctl->t_prev_end;
+  }
   den_pass_reduce(gpart, n_groups, F.nd, pass_out);
   __syncthreads();
   if (threadIdx.x == 0 && ph == kMinNewton) ctl->newton_parts[0] += clock64() - t0;
@@ -1596,6 +1985,8 @@ min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __
     counter[n_groups] = 0u;
     ctl->tail_cycles[ph == kMinNewton ? 0 : 1] += clock64() - t0;
     ctl->n_steps[ph == kMinNewton ? 0 : 1] += 1;
+    ctl->t_prev_end = global_ns();
+    ctl->tail_ns += ctl->t_prev_end - ctl->t_arrive;
   }
 }
 
@@ -1725,6 +2116,16 @@ cudaError_t fit_malloc(void** p, size_t bytes) {
   return g_fit_stream ? cudaMallocAsync(p, bytes, g_fit_stream) : cudaMalloc(p, bytes);
 }
 
+// RPG_FIT_PDL=0: minimizer steps launch without programmatic dependent
+// launch (each step's grid then starts only after the previous completes).
+static bool fit_use_pdl() {
+  static const bool on = [] {
+    const char* e = getenv("RPG_FIT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // RPG_FIT_NO_DMMA=1: the sample passes of nd <= 8 denominators use the
 // generic kernels (Gram of D/q with FMA chains) instead of the
 // register-resident nd = 8 path with the FP64 tensor-core Gram
@@ -1811,6 +2212,25 @@ int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, c
 
 }  // namespace
 
+// Where the nd <= 8 sample passes take a row's denominator monomials from.
+static int den_src(const FitParams& F) {
+  if (F.Dm) return kSrcDm;
+  if (F.den_lat3) return kSrcLat3;
+  if (F.den01) return kSrcMask;
+  return kSrcGeneric;
+}
+
+using DenPassFn = void (*)(const FitParams, const double*, const double*, const double*, int, int,
+                           double*, CtlSrc);
+static DenPassFn den_pass8_fn(int src) {
+  switch (src) {
+    case kSrcDm: return den_pass<8, kSrcDm>;
+    case kSrcLat3: return den_pass<8, kSrcLat3>;
+    case kSrcMask: return den_pass<8, kSrcMask>;
+    default: return den_pass<8, kSrcGeneric>;
+  }
+}
+
 size_t den_pass_smem(const FitParams& F) {
   const size_t ust = F.nd <= 8 ? 8 : (size_t)F.nd;
   return sizeof(double) * ((size_t)kPassRows * ust + 32 + kAlphas * (size_t)std::max(F.nd, 4)) +
@@ -1842,8 +2262,9 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
   }
   const size_t sm = den_pass_smem(F);
   if (F.nd <= 8 && fit_use_dmma()) {
-    FCUDA(raise_smem_attr(reinterpret_cast<const void*>(den_pass<8>), sm));
-    den_pass<8><<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>(), src);
+    const DenPassFn fn = den_pass8_fn(den_src(F));
+    FCUDA(raise_smem_attr(reinterpret_cast<const void*>(fn), sm));
+    fn<<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton, P->part.as<double>(), src);
   } else {
     FCUDA(raise_smem_attr(reinterpret_cast<const void*>(den_pass<kMaxCols>), sm));
     den_pass<kMaxCols><<<P->G, kFitThreads, sm, s>>>(F, cd, dd, alphas, n_alpha, newton,
@@ -1899,8 +2320,19 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   FCUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned) * (n_groups + 1), s));
   FCUDA(fit_malloc((void**)&gpart.p, sizeof(double) * (size_t)n_groups * Wp));
   const size_t smstep = std::max(smk, den_pass_smem(F));
-  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(min_step<8>), smstep));
-  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(min_step<kMaxCols>), smstep));
+  using MinStepFn = void (*)(const FitParams, CtlSrc, double*, double*, unsigned*, double*, const double*,
+                            const double*, const double*, double*, double*, MinCtl*, MinState*,
+                            const double*);
+  MinStepFn step_fn = min_step<kMaxCols>;
+  if (F.nd <= 8 && fit_use_dmma()) {
+    switch (den_src(F)) {
+      case kSrcDm: step_fn = min_step<8, kSrcDm>; break;
+      case kSrcLat3: step_fn = min_step<8, kSrcLat3>; break;
+      case kSrcMask: step_fn = min_step<8, kSrcMask>; break;
+      default: step_fn = min_step<8, kSrcGeneric>; break;
+    }
+  }
+  FCUDA(raise_smem_attr(reinterpret_cast<const void*>(step_fn), smstep));
   // Constant-block factorization for the Schur-complement Newton solve.
   DevBuf prepb;
   FCUDA(fit_malloc((void**)&prepb.p, sizeof(double) * (size_t)prep_size(nn, nd)));
@@ -1915,15 +2347,20 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   constexpr int kChunk = 24;
   for (int done = 0, steps = 0; !done && steps < 16 * 40 * 16; steps += kChunk) {
     for (int i = 0; i < kChunk; ++i) {
-      if (F.nd <= 8 && fit_use_dmma())
-        min_step<8><<<P.G, kFitThreads, smstep, s>>>(F, src, P.part.as<double>(), P.out.as<double>(),
-                                                     counter.as<unsigned>(), gpart.as<double>(), R, S,
-                                                     gsum, c.as<double>(), dc.as<double>(), dctl,
-                                                     st.as<MinState>(), prepb.as<double>());
-      else
-        min_step<kMaxCols><<<P.G, kFitThreads, smstep, s>>>(
-            F, src, P.part.as<double>(), P.out.as<double>(), counter.as<unsigned>(), gpart.as<double>(),
-            R, S, gsum, c.as<double>(), dc.as<double>(), dctl, st.as<MinState>(), prepb.as<double>());
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(P.G);
+      cfg.blockDim = dim3(kFitThreads);
+      cfg.dynamicSmemBytes = smstep;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = fit_use_pdl() ? 1 : 0;
+      FCUDA(cudaLaunchKernelEx(&cfg, step_fn, F,
+                               src, P.part.as<double>(), P.out.as<double>(), counter.as<unsigned>(),
+                               gpart.as<double>(), R, S, gsum, c.as<double>(), dc.as<double>(), dctl,
+                               st.as<MinState>(), (const double*)prepb.as<double>()));
     }
     FCUDA(cudaGetLastError());
     FCUDA(cudaMemcpyAsync(&hc, ctlb.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
@@ -1944,6 +2381,11 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
     if (done && getenv("RPG_FIT_TRACE") && hc.n_steps[0])
       fprintf(stderr, "[rpg_fit]   Newton tail: final fold %.1f us, solve %.1f us (rest: staging, control)\n",
               hc.newton_parts[0] / 1965.0 / hc.n_steps[0], hc.newton_parts[2] / 1965.0 / hc.n_steps[0]);
+    if (done && getenv("RPG_FIT_TRACE") && hc.n_steps[0] + hc.n_steps[1] > 1)
+      fprintf(stderr, "[rpg_fit]   per step: sample pass %.1f us, tail %.1f us, inter-step gap %.1f us\n",
+              1e-3 * hc.pass_ns / (hc.n_steps[0] + hc.n_steps[1]),
+              1e-3 * hc.tail_ns / (hc.n_steps[0] + hc.n_steps[1]),
+              1e-3 * hc.gap_ns / (hc.n_steps[0] + hc.n_steps[1] - 1));
   }
   if (hc.phase == kMinFail) return RPG_OK;
   to_raw<<<1, 32, 0, s>>>(c.as<double>(), S, n, out_raw, fin.as<int>());
@@ -1963,7 +2405,12 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
   // The sample passes read precomputed denominator monomials.
   DevBuf dm;
   FitParams F = F0;
-  static const bool use_dm = getenv("RPG_FIT_NO_DM") == nullptr;
+  // RPG_FIT_DM=1 forces the precomputed monomials, RPG_FIT_DM=0 forbids
+  // them; by default they are skipped when the pass recomputes them from x
+  // by bit masks (den01, no HBM pass over an m x 8 array).
+  static const char* dm_env = getenv("RPG_FIT_DM");
+  static const bool no_dm_env = getenv("RPG_FIT_NO_DM") != nullptr;
+  const bool use_dm = !no_dm_env && (dm_env ? dm_env[0] == '1' : !(F0.den01 && nd <= 8));
   if (use_dm && fit_malloc((void**)&dm.p, sizeof(double) * (size_t)F0.m * (nd <= 8 ? 8 : nd)) == cudaSuccess) {
     den_monomials<<<(int)std::min<int64_t>((F0.m + 255) / 256, 8LL * sms), 256, 0, s>>>(
         F0, dm.as<double>());
@@ -2147,6 +2594,18 @@ int fit_impl(const double* X, const double* dXs, const double* y, int64_t m, int
   F.w = nullptr;
   F.exps = dexps.as<uint8_t>();
   F.m = m;
+  F.den01 = n_vars <= 4;
+  for (size_t e = (size_t)nn * n_vars; e < exps.size(); ++e)
+    if (exps[e] > 1) F.den01 = 0;
+  {
+    // monomial_basis({1, 1, 1}) (polyfit.hpp:50-73), the den_pass kSrcLat3 order
+    static const uint8_t lat3[8][3] = {{0, 0, 0}, {0, 0, 1}, {0, 1, 0}, {1, 0, 0},
+                                       {0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {1, 1, 1}};
+    F.den_lat3 = n_vars == 3 && nd == 8;
+    for (int k = 0; F.den_lat3 && k < 8; ++k)
+      for (int v = 0; v < 3; ++v)
+        if (exps[(size_t)(nn + k) * 3 + v] != lat3[k][v]) F.den_lat3 = 0;
+  }
   // RPG_FIT_TRACE=1: per-phase wall times on stderr (profiling aid).
   const bool phase_trace = getenv("RPG_FIT_TRACE") != nullptr;
   auto t_prev = std::chrono::steady_clock::now();

@@ -196,3 +196,45 @@ def test_multi_fit_equals_one_by_one():
         assert gf.num.coeffs == f.num.coeffs and gf.den.coeffs == f.den.coeffs
         assert grep.singular_values == rep.singular_values
         assert (grep.numerical_rank, grep.safeguard, grep.truncated) == (rep.numerical_rank, rep.safeguard, rep.truncated)
+
+
+_DM_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import bench
+from paper_1906_00142_b200 import fit as G
+X, ys, variables = bench.c4_data(200000, 0.01)
+out = {}
+for name in sorted(ys):
+    tr = {}
+    try:
+        f, rep = G.fit_rational(X, ys[name], variables, [2, 2, 2], [1, 1, 1], trace=tr)
+        res = [float(c).hex() for c in list(f.num.coeffs) + list(f.den.coeffs)] + [rep.safeguard]
+    except (G.DegenerateFit, G.SvdFailure) as e:
+        res = [type(e).__name__]
+    out[name] = [res, [[float(v).hex() for v in st] for st in tr.get("stages", [])]]
+print(json.dumps(out))
+"""
+
+
+def test_den_pass_monomial_sources_bit_identical():
+    """The safeguard's sample passes take the denominator monomials either
+    from a precomputed m x 8 array (RPG_FIT_DM=1) or recompute them from x by
+    exponent bit masks (RPG_FIT_DM=0, the default for 0/1 denominator
+    exponents): the two are the same products in the same order, so every
+    stage vector and every fitted coefficient is bit-identical."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = []
+    for mode in ("0", "1"):
+        env = dict(os.environ, RPG_FIT_DM=mode)
+        p = subprocess.run([sys.executable, "-c", _DM_SCRIPT, root], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        runs.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    assert runs[0] == runs[1]
+    assert any(v[0][-1] is True for v in runs[0].values())  # the safeguard ran

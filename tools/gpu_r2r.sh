@@ -1,0 +1,18 @@
+#!/bin/bash
+# Fit: programmatic dependent launch of the minimizer steps (A/B RPG_FIT_PDL=0),
+# bit A/B vs the previous build, step anatomy, timings, fit tests.
+set -u
+TAG=${1:-r02r}
+O=gpurun_out/$TAG
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build rc=$?"
+echo "== bits vs old"; timeout 1200 python tools/fit_ab_bits.py build/old_librpgpu.so > $O/ab_bits.log 2>&1; tail -1 $O/ab_bits.log
+for pdl in 1 0; do
+  echo "== pdl=$pdl"
+  RPG_FIT_PDL=$pdl RPG_FIT_TRACE=1 timeout 900 python tools/bench_fit.py --reps 1 --noise 0.01 --no-warmup > $O/trace_pdl$pdl.log 2>&1
+  grep -E 'wall|per step|tail' $O/trace_pdl$pdl.log | head -6
+  RPG_FIT_PDL=$pdl timeout 900 python tools/bench_fit.py --reps 3 --noise 0.01 > $O/bench_noisy_pdl$pdl.log 2>&1
+  RPG_FIT_PDL=$pdl timeout 900 python tools/bench_fit.py --reps 3 > $O/bench_clean_pdl$pdl.log 2>&1
+  for f in bench_noisy_pdl$pdl bench_clean_pdl$pdl; do tail -1 $O/$f.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$f seq %.1f ms multi %.1f ms' % (1e3*d['gpu_seconds'], 1e3*d['multi_seconds']))"; done
+done
+echo "== pytest"; timeout 1800 python -m pytest tests/test_gpu_fit.py tests/test_gpu_fit_c4.py -q -m gpu > $O/pytest_gpu.log 2>&1; echo "rc=$?"; tail -3 $O/pytest_gpu.log
