@@ -14,7 +14,8 @@ import numpy as np
 from . import formats as F
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librpgpu.so")
+# RPG_LIBRARY: another build of librpgpu.so (A/B measurements of build variants)
+LIB_PATH = os.environ.get("RPG_LIBRARY") or os.path.join(HERE, "librpgpu.so")
 
 RPG_MAX_VARS = 8
 RPG_N_METRICS = 7

@@ -559,8 +559,50 @@ __global__ void den_monomials(const FitParams F, double* __restrict__ Dm) {
   }
 }
 
-// NDT: compile-time bound on nd (8 = the default (1,1,1) denominator basis)
-// so the per-row monomials and accumulators stay in registers.
+// Per-candidate min q and sum log q of the CTA's rows into out[2a], out[2a+1]
+// (warp shuffles, then warps 0..7 in order; buf: >= 2 kAlphas kFitWarps
+// doubles of SMEM free after the leading barrier).
+__device__ __forceinline__ void write_alpha_partials(const double (&qmin)[kAlphas],
+                                                     const double (&slog)[kAlphas], double* buf,
+                                                     double* out) {
+  double t[kAlphas], u[kAlphas];
+#pragma unroll
+  for (int a = 0; a < kAlphas; ++a) {
+    t[a] = qmin[a];
+    u[a] = slog[a];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int a = 0; a < kAlphas; ++a) {
+      t[a] = fmin(t[a], __shfl_xor_sync(0xffffffffu, t[a], o));
+      u[a] += __shfl_xor_sync(0xffffffffu, u[a], o);
+    }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < kAlphas; ++a) {
+      buf[a * 2 * kFitWarps + (threadIdx.x >> 5)] = t[a];
+      buf[a * 2 * kFitWarps + kFitWarps + (threadIdx.x >> 5)] = u[a];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kAlphas) {
+    const double* b = buf + threadIdx.x * 2 * kFitWarps;
+    double mn = b[0], sm = b[kFitWarps];
+    for (int i = 1; i < kFitWarps; ++i) {
+      mn = fmin(mn, b[i]);
+      sm += b[kFitWarps + i];
+    }
+    out[2 * threadIdx.x] = mn;
+    out[2 * threadIdx.x + 1] = sm;
+  }
+}
+
+// The sample pass for any nd <= NDT (the FMA Gram; nd <= 8 runs
+// den_pass8_body unless RPG_FIT_NO_DMMA): per CTA, for each candidate a,
+// min q and sum log q over its rows, and with `newton` for candidate 0 also
+// sum (1/q) D_k and sum (1/q^2) D_k D_k^T.
 template <int NDT>
 __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* __restrict__ cd,
                                               const double* __restrict__ dd,
@@ -577,33 +619,13 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
     newton = ph == kMinNewton;
     n_alpha = newton ? 1 : src.ctl->n_alpha;
   }
+  const int ust = nd <= 8 ? 8 : nd;                 // row stride of U and of Dm (den_pass_smem)
   double* U = fsm;                                  // kPassRows x ust (row-major)
-  const int ust = NDT == 8 ? 8 : nd;                // row stride (8: padded for the DMMA Gram)
-  double* red = U + kPassRows * ust;                // 32
-  double* cands = red + 32;                         // kAlphas x nd (NDT == 8: cd[8], dd[8])
+  double* cands = U + kPassRows * ust + 32;         // kAlphas x nd
   uint8_t* sexps = reinterpret_cast<uint8_t*>(cands + kAlphas * (nd > 4 ? nd : 4));
   for (int e = threadIdx.x; e < nd * F.n_vars; e += blockDim.x)
     sexps[e] = F.exps[F.nn * F.n_vars + e];
-  double al[kAlphas] = {0.0, 0.0, 0.0, 0.0};
-  bool has_dir = false;
-  if constexpr (NDT == 8) {
-    // q_a = D.(cd + al_a dd) evaluated as D.cd + al_a (D.dd): two dot products
-    // per row for all candidates.
-    has_dir = src.ctl ? !newton : dd != nullptr;
-#pragma unroll
-    for (int a = 0; a < kAlphas; ++a)
-      al[a] = a < n_alpha ? (src.ctl ? src.ctl->al[a] : (alphas ? alphas[a] : 0.0)) : 0.0;
-    if (threadIdx.x < 16) {
-      const int k = threadIdx.x & 7;
-      double v = 0.0;
-      if (k < nd) {
-        if (threadIdx.x < 8) v = src.ctl ? src.S[F.nn + k] * src.c[F.nn + k] : cd[k];
-        else if (has_dir) v = src.ctl ? src.S[F.nn + k] * src.dc[F.nn + k] : dd[k];
-      }
-      cands[threadIdx.x] = v;
-    }
-  }
-  for (int e = threadIdx.x; NDT != 8 && e < n_alpha * nd; e += blockDim.x) {
+  for (int e = threadIdx.x; e < n_alpha * nd; e += blockDim.x) {
     const int a = e / nd, k = e % nd;
     if (src.ctl) {
       const int j = F.nn + k;
@@ -629,133 +651,20 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
   const int parts = (nd * nd <= (int)blockDim.x / 2) ? (int)blockDim.x / (nd * nd) >= 4 ? 4 : 2 : 1;
   const int ne_stride = parts > 1 ? nd * nd : (int)blockDim.x;
   const int part = parts > 1 ? (int)threadIdx.x / (nd * nd) : 0;
-  double gacc[NDT <= 8 ? 1 : 16];
+  double gacc[16];
 #pragma unroll
-  for (int i = 0; i < (NDT <= 8 ? 1 : 16); ++i) gacc[i] = 0.0;
+  for (int i = 0; i < 16; ++i) gacc[i] = 0.0;
   double gq = 0.0;  // thread t < nd owns sum (1/q) D[t]
-  double gmma0 = 0.0, gmma1 = 0.0, gqv = 0.0;  // NDT == 8: DMMA accumulator fragment, column sums
   const int64_t nrow_tiles = (F.m + kPassRows - 1) / kPassRows;
-  // NDT == 8 with precomputed monomials: the next tile's row is loaded
-  // while the current one is processed (a CTA walks ~7 tiles; without the
-  // prefetch every tile exposes a full DRAM round trip).
-  double2 pre[4];
-  // den01 without Dm: the monomials are recomputed from x by bit masks
-  // (4 bits per monomial, bit v = exponent 1 on variable v), x of the next
-  // tile prefetched into pre[0..1].
-  const bool x01 = NDT == 8 && !F.Dm && F.den01;
-  uint32_t dm4 = 0;
-  bool lattice3 = false;
-  if (x01) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-        if (k < nd && v < F.n_vars && sexps[k * F.n_vars + v]) dm4 |= 1u << (4 * k + v);
-    // monomial_basis({1, 1, 1}) (polyfit.hpp:50-73): 1, x2, x1, x0, x1x2,
-    // x0x2, x0x1, x0x1x2 — bit v of each nibble = exponent of x_v
-    lattice3 = nd == 8 && F.n_vars == 3 && dm4 == 0x73561240u;
-    const int64_t r0 = (int64_t)blockIdx.x * kPassRows + threadIdx.x;
-    pre[0] = pre[1] = make_double2(0.0, 0.0);
-    if (blockIdx.x < nrow_tiles && threadIdx.x < kPassRows && r0 < F.m) {
-      const double* xr = F.X + r0 * F.n_vars;
-      pre[0].x = xr[0];
-      if (F.n_vars > 1) pre[0].y = xr[1];
-      if (F.n_vars > 2) pre[1].x = xr[2];
-      if (F.n_vars > 3) pre[1].y = xr[3];
-    }
-  }
-  if (NDT == 8 && F.Dm) {
-    const int64_t r0 = (int64_t)blockIdx.x * kPassRows + threadIdx.x;
-    if (blockIdx.x < nrow_tiles && threadIdx.x < kPassRows && r0 < F.m) {
-      const double2* row = reinterpret_cast<const double2*>(F.Dm + r0 * 8);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) pre[k] = row[k];
-    }
-  }
   for (int64_t tile = blockIdx.x; tile < nrow_tiles; tile += gridDim.x) {
     const int64_t r = tile * kPassRows + threadIdx.x;
     const bool valid = threadIdx.x < kPassRows && r < F.m;
     double D[NDT];
-    if (NDT == 8 && valid) {
+    if (valid) {
       if (F.Dm) {
+        // Denominator monomials precomputed once per fit (m x ust).
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          D[2 * k] = pre[k].x;
-          D[2 * k + 1] = pre[k].y;
-        }
-        const int64_t rn = (tile + gridDim.x) * kPassRows + threadIdx.x;
-        if (tile + gridDim.x < nrow_tiles && rn < F.m) {
-          const double2* row = reinterpret_cast<const double2*>(F.Dm + rn * 8);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) pre[k] = row[k];
-        }
-      } else if (x01) {
-        // monomial()'s product order with the exponent-0 factors (exact
-        // multiplications by 1) skipped.
-        const double x[4] = {pre[0].x, pre[0].y, pre[1].x, pre[1].y};
-        if (lattice3) {
-          // the full {0,1}^3 basis in monomial_basis order: every product
-          // extends a shorter one by its highest variable, as monomial()
-          // multiplies (((1 x0) x1) x2) — 4 multiplies per row
-          const double p01 = x[0] * x[1], p02 = x[0] * x[2], p12 = x[1] * x[2];
-          D[0] = 1.0;
-          D[1] = x[2];
-          D[2] = x[1];
-          D[3] = x[0];
-          D[4] = p12;
-          D[5] = p02;
-          D[6] = p01;
-          D[7] = p01 * x[2];
-        } else {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            double mo = 1.0;
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              if ((dm4 >> (4 * k + v)) & 1u) mo *= x[v];
-            D[k] = k < nd ? mo : 0.0;
-          }
-        }
-        const int64_t rn = (tile + gridDim.x) * kPassRows + threadIdx.x;
-        if (tile + gridDim.x < nrow_tiles && rn < F.m) {
-          const double* xr = F.X + rn * F.n_vars;
-          pre[0].x = xr[0];
-          if (F.n_vars > 1) pre[0].y = xr[1];
-          if (F.n_vars > 2) pre[1].x = xr[2];
-          if (F.n_vars > 3) pre[1].y = xr[3];
-        }
-      } else {
-        double x[RPG_MAX_VARS];
-#pragma unroll
-        for (int v = 0; v < RPG_MAX_VARS; ++v) x[v] = v < F.n_vars ? F.X[r * F.n_vars + v] : 0.0;
-#pragma unroll
-        for (int k = 0; k < NDT; ++k) D[k] = k < nd ? monomial(x, sexps + k * F.n_vars, F.n_vars) : 0.0;
-      }
-      double q0 = 0.0, qd = 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) q0 = fma(D[k], cands[k], q0);
-      if (has_dir) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) qd = fma(D[k], cands[8 + k], qd);
-      }
-#pragma unroll
-      for (int a = 0; a < kAlphas; ++a) {
-        if (a < n_alpha) {
-          const double q = has_dir ? fma(al[a], qd, q0) : q0;
-          qmin[a] = fmin(qmin[a], q);
-          // mid-range q multiplies in unsplit: prod stays a power-of-two
-          // multiple of the normalized product and every multiply rounds
-          // on normal numbers, so the mantissa / exponent sums are those
-          // of splitting every factor
-          if (mid_range(q)) prod[a] *= q;
-          else prod[a] *= split_mant(q, pexp[a]);
-        }
-      }
-    } else if (valid) {
-      if (F.Dm) {
-        // Denominator monomials precomputed once per fit (m x nd).
-#pragma unroll
-        for (int k = 0; k < NDT; ++k) D[k] = k < nd ? F.Dm[r * nd + k] : 0.0;
+        for (int k = 0; k < NDT; ++k) D[k] = k < nd ? F.Dm[r * ust + k] : 0.0;
       } else {
         double x[RPG_MAX_VARS];
 #pragma unroll
@@ -782,8 +691,7 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
       }
     }
 #pragma unroll
-    for (int a = 0; a < kAlphas; ++a)  // keep products in range
-      if (NDT != 8 || !mid_range(prod[a])) prod[a] = split_mant(prod[a], pexp[a]);
+    for (int a = 0; a < kAlphas; ++a) prod[a] = split_mant(prod[a], pexp[a]);  // keep products in range
     if (newton) {
       __syncthreads();
       if (threadIdx.x < kPassRows) {
@@ -791,34 +699,14 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
         if (valid) {
 #pragma unroll
           for (int k = 0; k < NDT; ++k)
-            if (NDT == 8 || k < nd) q = fma(D[k], cands[k], q);
+            if (k < nd) q = fma(D[k], cands[k], q);
           qi = 1.0 / q;
         }
-        if constexpr (NDT == 8) {
-          // stride 8, zero-padded past nd (the DMMA Gram below)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) U[threadIdx.x * 8 + k] = (valid && k < nd) ? D[k] * qi : 0.0;
-        } else {
-#pragma unroll
-          for (int k = 0; k < NDT; ++k)
-            if (k < nd) U[threadIdx.x * nd + k] = valid ? D[k] * qi : 0.0;
-        }
+        for (int k = 0; k < NDT; ++k)
+          if (k < nd) U[threadIdx.x * ust + k] = valid ? D[k] * qi : 0.0;
       }
       __syncthreads();
-      if constexpr (NDT == 8) {
-        // Gram U^T U and column sums on the FP64 tensor cores: warp w folds
-        // rows [32w, 32w + 32) in 4-row chunks with mma.m8n8k4 (A = U^T
-        // chunk, B = U chunk: lane l supplies U[r0 + l%4][l/4] to both).
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-        for (int cidx = 0; cidx < 8; ++cidx) {
-          const double v = U[(warp * 32 + cidx * 4 + (lane & 3)) * 8 + (lane >> 2)];
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                       : "+d"(gmma0), "+d"(gmma1) : "d"(v), "d"(v));
-          gqv += v;
-        }
-        continue;
-      }
       // Gram of the tile's U rows: `parts` threads per entry, each over a
       // contiguous row range with four independent accumulators.
       for (int e = threadIdx.x % ne_stride, i = 0; part < parts && e < nd * nd; e += ne_stride, ++i) {
@@ -826,49 +714,27 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
         const int r0 = part * (kPassRows / parts), r1 = r0 + kPassRows / parts;
         double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
         for (int row = r0; row < r1; row += 4) {
-          t0 = fma(U[row * nd + a], U[row * nd + b], t0);
-          t1 = fma(U[(row + 1) * nd + a], U[(row + 1) * nd + b], t1);
-          t2 = fma(U[(row + 2) * nd + a], U[(row + 2) * nd + b], t2);
-          t3 = fma(U[(row + 3) * nd + a], U[(row + 3) * nd + b], t3);
+          t0 = fma(U[row * ust + a], U[row * ust + b], t0);
+          t1 = fma(U[(row + 1) * ust + a], U[(row + 1) * ust + b], t1);
+          t2 = fma(U[(row + 2) * ust + a], U[(row + 2) * ust + b], t2);
+          t3 = fma(U[(row + 3) * ust + a], U[(row + 3) * ust + b], t3);
         }
-        if (NDT <= 8) gacc[0] += (t0 + t1) + (t2 + t3);
-        else gacc[i] += (t0 + t1) + (t2 + t3);
+        gacc[i] += (t0 + t1) + (t2 + t3);
       }
       if ((int)threadIdx.x < nd) {
         // sum_k (1/q_k) D_k[t] = sum of column t of U
         double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
         for (int row = 0; row < kPassRows; row += 4) {
-          t0 += U[row * nd + threadIdx.x];
-          t1 += U[(row + 1) * nd + threadIdx.x];
-          t2 += U[(row + 2) * nd + threadIdx.x];
-          t3 += U[(row + 3) * nd + threadIdx.x];
+          t0 += U[row * ust + threadIdx.x];
+          t1 += U[(row + 1) * ust + threadIdx.x];
+          t2 += U[(row + 2) * ust + threadIdx.x];
+          t3 += U[(row + 3) * ust + threadIdx.x];
         }
         gq += (t0 + t1) + (t2 + t3);
       }
     }
   }
-  if constexpr (NDT == 8) {
-    if (newton) {
-      // Fold the 8 warps' fragments (fixed order): thread t holds
-      // G[t/4][2(t%4) + {0,1}] of its warp; column sums by column t/4.
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      gqv += __shfl_xor_sync(0xffffffffu, gqv, 1);
-      gqv += __shfl_xor_sync(0xffffffffu, gqv, 2);
-      __syncthreads();
-      double* Pm = U;  // reuse: 8 warps x (64 Gram + 8 column sums)
-      Pm[warp * 72 + (lane >> 2) * 8 + 2 * (lane & 3)] = gmma0;
-      Pm[warp * 72 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = gmma1;
-      if ((lane & 3) == 0) Pm[warp * 72 + 64 + (lane >> 2)] = gqv;
-      __syncthreads();
-      if (threadIdx.x < 72) {
-        double t = 0.0;
-        for (int w = 0; w < kFitWarps; ++w) t += Pm[w * 72 + threadIdx.x];
-        if (threadIdx.x < 64) gacc[0] = t;
-        else gq = t;
-      }
-    }
-  }
-  if (newton && parts > 1 && NDT != 8) {
+  if (newton && parts > 1) {
     // Fold the per-part partial Gram entries (thread = part * ne + entry).
     __syncthreads();
     double* P = U;  // reuse: parts x nd*nd
@@ -881,47 +747,15 @@ __device__ __forceinline__ void den_pass_body(const FitParams& F, const double* 
     }
   }
 #pragma unroll
-  for (int a = 0; a < kAlphas; ++a) {
-    // normalized as after the per-tile split of every tile (CTAs past the
-    // last tile never split: prod 1, exponent 0)
-    if (NDT == 8 && (int64_t)blockIdx.x < nrow_tiles) prod[a] = split_mant(prod[a], pexp[a]);
-    slog[a] = fma((double)pexp[a], 0.69314718055994530942, log(prod[a]));
-  }
+  for (int a = 0; a < kAlphas; ++a) slog[a] = fma((double)pexp[a], 0.69314718055994530942, log(prod[a]));
   double* out = partial + (size_t)blockIdx.x * (2 * kAlphas + nd + nd * nd);
-#pragma unroll
-  for (int a = 0; a < kAlphas; ++a) {
-    double t = qmin[a], u = slog[a];
-    for (int o = 16; o > 0; o >>= 1) {
-      t = fmin(t, __shfl_xor_sync(0xffffffffu, t, o));
-      u += __shfl_xor_sync(0xffffffffu, u, o);
-    }
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) {
-      red[threadIdx.x >> 5] = t;
-      red[16 + (threadIdx.x >> 5)] = u;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double mn = red[0], sm = red[16];
-      for (int i = 1; i < kFitWarps; ++i) {
-        mn = fmin(mn, red[i]);
-        sm += red[16 + i];
-      }
-      out[2 * a] = mn;
-      out[2 * a + 1] = sm;
-    }
-  }
-  if (newton && NDT == 8) {
-    const int t = threadIdx.x;
-    if (t < 64 && (t >> 3) < nd && (t & 7) < nd) out[2 * kAlphas + nd + (t >> 3) * nd + (t & 7)] = gacc[0];
-    if (t >= 64 && t < 64 + nd) out[2 * kAlphas + (t - 64)] = gq;
-  } else if (newton) {
+  write_alpha_partials(qmin, slog, U + (size_t)parts * nd * nd, out);
+  if (newton) {
     if ((int)threadIdx.x < nd) out[2 * kAlphas + threadIdx.x] = gq;
     if (parts > 1) {
       if ((int)threadIdx.x < nd * nd) out[2 * kAlphas + nd + threadIdx.x] = gacc[0];
     } else {
-      for (int e = threadIdx.x, i = 0; e < nd * nd; e += blockDim.x, ++i)
-        out[2 * kAlphas + nd + e] = gacc[NDT <= 8 ? 0 : i];
+      for (int e = threadIdx.x, i = 0; e < nd * nd; e += blockDim.x, ++i) out[2 * kAlphas + nd + e] = gacc[i];
     }
   }
 }
@@ -1075,46 +909,6 @@ __device__ __forceinline__ void rows8(const FitParams& F, int64_t nrow_tiles, co
   }
 }
 
-// Per-candidate min q and sum log q of the CTA's rows into out[2a], out[2a+1]
-// (warp shuffles, then warps 0..7 in order; buf: >= 2 kAlphas kFitWarps
-// doubles of SMEM free after the leading barrier).
-__device__ __forceinline__ void write_alpha_partials(const double (&qmin)[kAlphas],
-                                                     const double (&slog)[kAlphas], double* buf,
-                                                     double* out) {
-  double t[kAlphas], u[kAlphas];
-#pragma unroll
-  for (int a = 0; a < kAlphas; ++a) {
-    t[a] = qmin[a];
-    u[a] = slog[a];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int a = 0; a < kAlphas; ++a) {
-      t[a] = fmin(t[a], __shfl_xor_sync(0xffffffffu, t[a], o));
-      u[a] += __shfl_xor_sync(0xffffffffu, u[a], o);
-    }
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int a = 0; a < kAlphas; ++a) {
-      buf[a * 2 * kFitWarps + (threadIdx.x >> 5)] = t[a];
-      buf[a * 2 * kFitWarps + kFitWarps + (threadIdx.x >> 5)] = u[a];
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < kAlphas) {
-    const double* b = buf + threadIdx.x * 2 * kFitWarps;
-    double mn = b[0], sm = b[kFitWarps];
-    for (int i = 1; i < kFitWarps; ++i) {
-      mn = fmin(mn, b[i]);
-      sm += b[kFitWarps + i];
-    }
-    out[2 * threadIdx.x] = mn;
-    out[2 * threadIdx.x + 1] = sm;
-  }
-}
-
 template <int SRC>
 __device__ __forceinline__ void den_pass8_body(const FitParams& F, const double* __restrict__ cd,
                                                const double* __restrict__ dd,
@@ -1226,9 +1020,11 @@ den_pass(const FitParams F, const double* __restrict__ cd, const double* __restr
 // back, one L2 round trip for the whole fold instead of one per value), a
 // fixed g order (deterministic).
 __device__ __forceinline__ void den_pass_reduce(const double* __restrict__ partial, int G, int nd,
-                                                double* __restrict__ out) {
+                                                double* __restrict__ out, bool newton) {
   const int W = 2 * kAlphas + nd + nd * nd;
-  for (int e = threadIdx.x; e < W; e += blockDim.x) {
+  // a non-Newton pass writes only the candidates' (min q, sum log q)
+  const int nv = newton ? W : 2 * kAlphas;
+  for (int e = threadIdx.x; e < nv; e += blockDim.x) {
     const bool is_min = e < 2 * kAlphas && (e % 2) == 0;
     double t = is_min ? INFINITY : 0.0;
     const double* p = partial + e;
@@ -1246,9 +1042,9 @@ __device__ __forceinline__ void den_pass_reduce(const double* __restrict__ parti
 }
 
 __global__ void den_pass_final(const double* __restrict__ partial, int G, int nd,
-                               double* __restrict__ out, const MinCtl* __restrict__ ctl) {
+                               double* __restrict__ out, const MinCtl* __restrict__ ctl, int newton) {
   if (ctl && ctl->phase >= kMinDone) return;
-  den_pass_reduce(partial, G, nd, out);
+  den_pass_reduce(partial, G, nd, out, ctl ? ctl->phase == kMinNewton : newton != 0);
 }
 
 // ||R S v||^2 for the n x n upper-triangular R (row-major) and scale S.
@@ -1301,6 +1097,15 @@ __global__ void min_setup(const double* __restrict__ R, const double* __restrict
 constexpr int kPrepOk = 0;
 __host__ __device__ inline int prep_size(int nn, int nd) {
   return 1 + nn * nn + 2 * nn * nd + nd * nd;
+}
+
+// Doubles of SMEM the Newton step's workspace takes ahead of the staged R
+// and prep factors: newton_body's KKT system (N x (N+1) + 3n) or
+// newton_schur_fast's fixed layout (kSchurWs), whichever is larger.
+constexpr int kSchurWs = 504;
+__host__ __device__ inline int newton_ws(int n) {
+  const int kkt = (n + 1) * (n + 2) + 3 * n;
+  return kkt > kSchurWs ? kkt : kSchurWs;
 }
 
 __global__ void __launch_bounds__(kFitThreads)
@@ -1557,7 +1362,7 @@ __device__ void newton_schur_fast(const double* R, const double* __restrict__ S,
     if (lane == 0) st->ok = sing ? 0 : 1;
   }
   __syncthreads();
-  double* dcs = ws + 440;     // 64: dc, also kept here for the decrement
+  double* dcs = ws + 440;     // 64: dc, also kept here for the decrement (440 + 64 = kSchurWs)
   for (int i = threadIdx.x; i < nn; i += blockDim.x) {
     double t = tu[i];
     for (int j = 0; j < nd; ++j) t -= Fm[i * nd + j] * xs[j];
@@ -1834,15 +1639,18 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
   // product below reads it many times.
   {
     extern __shared__ __align__(16) double fsm[];
-    double* Rs = fsm + (n + 1) * (n + 2) + 3 * n;  // behind newton_body's workspace
+    double* Rs = fsm + newton_ws(n);               // behind the Newton step's workspace
     double* Ps = Rs + n * n;                       // the min_prep factors
     __syncthreads();
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) Rs[e] = R[e];
-    if (prep && ph == kMinNewton)
+    // the prep factors only when min_prep succeeded (else only the flag is
+    // written and newton_body takes the general path)
+    const bool stage_prep = prep && ph == kMinNewton && prep[kPrepOk] != 0.0;
+    if (stage_prep)
       for (int e = threadIdx.x; e < prep_size(nn, nd); e += blockDim.x) Ps[e] = prep[e];
     __syncthreads();
     R = Rs;
-    if (prep && ph == kMinNewton) prep = Ps;
+    if (stage_prep) prep = Ps;
   }
   const long long t_staged = clock64();
   if (ph == kMinNewton) {
@@ -1930,8 +1738,11 @@ __device__ __forceinline__ void ctl_step_body(const double* R, const double* __r
 // arrives last.  No-op for every CTA once the loop is done.
 constexpr int kStepGroup = 32;
 
+#ifndef RPG_FIT_STEP_MINB
+#define RPG_FIT_STEP_MINB 2  // min_step CTAs per SM (launch bounds; the pass grid's default)
+#endif
 template <int NDT, int SRC = kSrcDm>
-__global__ void __launch_bounds__(kFitThreads, 2)
+__global__ void __launch_bounds__(kFitThreads, RPG_FIT_STEP_MINB)
 min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __restrict__ pass_out,
          unsigned* __restrict__ counter /* n_groups + 1 */, double* __restrict__ gpart,
          const double* __restrict__ R, const double* __restrict__ S,
@@ -1958,7 +1769,9 @@ min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __
   __syncthreads();
   if (!last) return;
   __threadfence();
-  den_pass_reduce(partial + (size_t)group * kStepGroup * W, gsize, F.nd, gpart + (size_t)group * W);
+  const bool newton_pass = src.ctl->phase == kMinNewton;  // only the tail below changes it
+  den_pass_reduce(partial + (size_t)group * kStepGroup * W, gsize, F.nd, gpart + (size_t)group * W,
+                  newton_pass);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1976,7 +1789,7 @@ min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __
     ctl->pass_ns += ctl->t_arrive - ts;
     if (ctl->t_prev_end) ctl->gap_ns += ts - ctl->t_prev_end;
   }
-  den_pass_reduce(gpart, n_groups, F.nd, pass_out);
+  den_pass_reduce(gpart, n_groups, F.nd, pass_out, ph == kMinNewton);
   __syncthreads();
   if (threadIdx.x == 0 && ph == kMinNewton) ctl->newton_parts[0] += clock64() - t0;
   ctl_step_body(R, S, gsum, pass_out, c, F.nn, F.nd, dc, ctl, scratch, prep);
@@ -2131,7 +1944,10 @@ static bool fit_use_pdl() {
 // register-resident nd = 8 path with the FP64 tensor-core Gram
 // (mma.m8n8k4.f64) — the A/B switch behind DESIGN.md's DMMA measurement.
 inline bool fit_use_dmma() {
-  static const bool on = getenv("RPG_FIT_NO_DMMA") == nullptr;
+  static const bool on = [] {
+    const char* e = getenv("RPG_FIT_NO_DMMA");
+    return e == nullptr || e[0] == '\0' || e[0] == '0';
+  }();
   return on;
 }
 
@@ -2253,7 +2069,7 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
     // reduction of the fused minimizer step).
     static const int per_sm = [] {
       const char* e = getenv("RPG_FIT_PASS_CTAS");
-      return e ? std::max(1, atoi(e)) : 2;  // min_step's launch bounds (r02k: 47 vs 51 ms at 3)
+      return e ? std::max(1, atoi(e)) : RPG_FIT_STEP_MINB;  // min_step's launch bounds
     }();
     P->G = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)per_sm * sms));
     P->nd = F.nd;
@@ -2271,7 +2087,7 @@ int run_den_pass(const FitParams& F, const double* cd, const double* dd, const d
                                                      P->part.as<double>(), src);
   }
   FCUDA(cudaGetLastError());
-  den_pass_final<<<1, 256, 0, s>>>(P->part.as<double>(), P->G, F.nd, P->out.as<double>(), src.ctl);
+  den_pass_final<<<1, 256, 0, s>>>(P->part.as<double>(), P->G, F.nd, P->out.as<double>(), src.ctl, newton);
   return RPG_OK;
 }
 
@@ -2303,8 +2119,7 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   FCUDA(cudaStreamSynchronize(s));
   if (!hs.ok) return RPG_OK;
   // newton_body's KKT workspace + the staged R (ctl_step_body)
-  const size_t smk = sizeof(double) * ((size_t)(n + 1) * (n + 2) + 3 * (size_t)n + (size_t)n * n +
-                                        (size_t)prep_size(nn, nd));
+  const size_t smk = sizeof(double) * ((size_t)newton_ws(n) + (size_t)n * n + (size_t)prep_size(nn, nd));
   DevBuf ctlb;
   FCUDA(fit_malloc((void**)&ctlb.p, sizeof(MinCtl)));
   MinCtl hc{};

@@ -238,3 +238,59 @@ def test_den_pass_monomial_sources_bit_identical():
         runs.append(json.loads(p.stdout.strip().splitlines()[-1]))
     assert runs[0] == runs[1]
     assert any(v[0][-1] is True for v in runs[0].values())  # the safeguard ran
+
+
+def target(P, cols):
+    """The acceptance target (acceptance.cpp:161-210) restricted to the
+    variables in cols: prod (v^2 + 1) / prod (v + 2), exactly representable
+    with bounds num 2 / den 1 per variable."""
+    t = np.ones(len(P))
+    for c in cols:
+        t = t * (P[:, c] ** 2 + 1) / (P[:, c] + 2)
+    return t
+
+
+_FMA_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1906_00142_b200 import fit as G
+from oracle import o3_fit as O3
+from tests.test_gpu_fit import target
+rng = np.random.default_rng(5150)
+P = rng.uniform(1.0, 4.0, (20000, 3))
+H = rng.uniform(1.0, 4.0, (50, 3))
+e = rng.uniform(-0.01, 0.01, len(P))
+out = {}
+for name, cols, bounds in (("xyz", [0, 1, 2], ([2, 2, 2], [1, 1, 1])), ("xy", [0, 1], ([2, 2], [1, 1]))):
+    noisy = target(P, cols) * (1 + e)
+    f, rep = G.fit_rational(P[:, cols], noisy, ["x", "y", "z"][:len(cols)], *bounds)
+    out[name] = [rep.safeguard, [float(v) for v in O3.eval_ratfunc(f, H[:, cols])]]
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("no_dmma", ["1", ""])
+def test_sample_pass_paths_match_o3(no_dmma):
+    """nd = 8 and nd = 4 fits with the safeguard running agree with O3 on
+    both sample-pass paths: the tensor-core one (den_pass8_body, default) and
+    the generic FMA-Gram one (den_pass_body, RPG_FIT_NO_DMMA=1)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", _FMA_SCRIPT, root], env=dict(os.environ, RPG_FIT_NO_DMMA=no_dmma),
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    got = json.loads(p.stdout.strip().splitlines()[-1])
+    rng = np.random.default_rng(5150)
+    P = rng.uniform(1.0, 4.0, (20000, 3))
+    H = rng.uniform(1.0, 4.0, (50, 3))
+    e = rng.uniform(-0.01, 0.01, len(P))
+    for name, cols, bounds in (("xyz", [0, 1, 2], ([2, 2, 2], [1, 1, 1])), ("xy", [0, 1], ([2, 2], [1, 1]))):
+        noisy = target(P, cols) * (1 + e)
+        fo, ro = O3.fit_rational(P[:, cols], noisy, ["x", "y", "z"][:len(cols)], *bounds)
+        assert got[name][0] == ro.safeguard
+        oh = ev(fo, H[:, cols])
+        assert np.max(np.abs(np.array(got[name][1]) - oh) / np.abs(oh)) < 1e-6, name

@@ -53,7 +53,12 @@ def main():
     a = ap.parse_args()
     o, n = run(a.old, a.samples), run(a.new, a.samples)
     diffs = [k for k in sorted(set(o) | set(n)) if o.get(k) != n.get(k)]
-    print(json.dumps({"identical": not diffs, "diffs": diffs, "n_fits": len(o)}))
+    first = {}
+    for k in diffs:  # the first safeguard stage whose vector differs (None: only the result)
+        so, sn = o.get(k, {}).get("stages", []), n.get(k, {}).get("stages", [])
+        first[k] = next((i for i in range(max(len(so), len(sn)))
+                         if i >= len(so) or i >= len(sn) or so[i] != sn[i]), None)
+    print(json.dumps({"identical": not diffs, "diffs": diffs, "first_stage": first, "n_fits": len(o)}))
 
 
 if __name__ == "__main__":
