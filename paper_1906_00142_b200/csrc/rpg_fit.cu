@@ -45,7 +45,10 @@ namespace rpg_fit {
 
 constexpr int kMaxCols = 64;   // n = |num basis| + |den basis|
 static_assert(kMaxCols == RPG_FIT_MAX_COLS, "rpg.h RPG_FIT_MAX_COLS");
-constexpr int kTile = 128;     // rows per SMEM tile
+#ifndef RPG_FIT_KTILE
+#define RPG_FIT_KTILE 256
+#endif
+constexpr int kTile = RPG_FIT_KTILE;  // rows per SMEM tile of the TSQR leaves
 constexpr int kFitThreads = 256;
 constexpr int kFitWarps = kFitThreads / 32;
 
@@ -507,7 +510,7 @@ struct MinCtl {
   // %globaltimer ns: CTA 0's start of the current step, end of the previous
   // step; summed sample-pass span (start -> last CTA's arrival) and
   // inter-step gap (previous end -> start).
-  unsigned long long t_start, t_prev_end, pass_ns, gap_ns, tail_ns, t_arrive;
+  unsigned long long t_start, t_prev_end, pass_ns, gap_ns, tail_ns, t_arrive, t_first;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -1755,7 +1758,10 @@ min_step(const FitParams F, CtlSrc src, double* __restrict__ partial, double* __
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (src.ctl->phase >= kMinDone) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_start = global_ns();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->t_start = global_ns();
+    if (!ctl->t_first) ctl->t_first = ctl->t_start;
+  }
   if constexpr (NDT == 8) den_pass8_body<SRC>(F, nullptr, nullptr, nullptr, 1, 1, partial, src);
   else den_pass_body<NDT>(F, nullptr, nullptr, nullptr, 1, 1, partial, src);
   const int W = 2 * kAlphas + F.nd + F.nd * F.nd;
@@ -1998,8 +2004,7 @@ int tsqr(const FitParams& F, int ncols, int sms, DevBuf* Rbuf, cudaStream_t s, c
   int per_sm = 1;
   FCUDA(raise_smem_attr(reinterpret_cast<const void*>(tsqr_tiles), sm1));
   FCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_tiles, kFitThreads, sm1));
-  (void)per_sm;
-  int G = (int)std::min<int64_t>(tiles, 4LL * sms);
+  int G = (int)std::min<int64_t>(tiles, (int64_t)std::max(1, std::min(per_sm, 4)) * sms);
   if (G < 1) G = 1;
   FCUDA(fit_malloc((void**)&Rbuf->p, sizeof(double) * (size_t)G * ncols * ncols));
   tsqr_tiles<<<G, kFitThreads, sm1, s>>>(F, Rbuf->as<double>());
@@ -2160,6 +2165,7 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
   // enqueued in chunks; the host only polls the phase between chunks.
   // Bound: 16 outer x 40 inner x (1 Newton + <= 15 line passes).
   constexpr int kChunk = 24;
+  const auto t_loop = std::chrono::steady_clock::now();
   for (int done = 0, steps = 0; !done && steps < 16 * 40 * 16; steps += kChunk) {
     for (int i = 0; i < kChunk; ++i) {
       cudaLaunchConfig_t cfg{};
@@ -2196,6 +2202,10 @@ int minimizer(const FitParams& F, const double* R, const double* S, const double
     if (done && getenv("RPG_FIT_TRACE") && hc.n_steps[0])
       fprintf(stderr, "[rpg_fit]   Newton tail: final fold %.1f us, solve %.1f us (rest: staging, control)\n",
               hc.newton_parts[0] / 1965.0 / hc.n_steps[0], hc.newton_parts[2] / 1965.0 / hc.n_steps[0]);
+    if (done && getenv("RPG_FIT_TRACE") && hc.n_steps[0] + hc.n_steps[1] > 1)
+      fprintf(stderr, "[rpg_fit]   host setup %.3f ms; device span first step -> last step end %.3f ms\n",
+              std::chrono::duration<double, std::milli>(t_loop - t_begin).count(),
+              1e-6 * (hc.t_prev_end - hc.t_first));
     if (done && getenv("RPG_FIT_TRACE") && hc.n_steps[0] + hc.n_steps[1] > 1)
       fprintf(stderr, "[rpg_fit]   per step: sample pass %.1f us, tail %.1f us, inter-step gap %.1f us\n",
               1e-3 * hc.pass_ns / (hc.n_steps[0] + hc.n_steps[1]),
@@ -2243,7 +2253,11 @@ int rpg_fit_safeguard(const FitParams& F0, const double* R, const double* S, dou
   FCUDA(raise_smem_attr(reinterpret_cast<const void*>(den_colsum), smc));
   den_colsum<<<G, kFitThreads, smc, s>>>(F, gpart.as<double>());
   sum_partials<<<1, 64, 0, s>>>(gpart.as<double>(), G, nd, gsum.as<double>());
-  // start vector: least squares of the numerator basis against y
+  // start vector: least squares of the numerator basis against y, from a
+  // QR of [V | y] of its own.  (The leading block of A's R is the same QR
+  // in exact arithmetic, but the start vector's rank truncation and the
+  // minimizer it seeds are sensitive to its rounding on rank-deficient C4
+  // metrics — r02aa: coal_mem_insts_per_thread parted from O3 at stage 1.)
   FitParams Fv = F;
   Fv.num_only = 1;
   Fv.with_y_col = 1;
