@@ -119,6 +119,53 @@ __device__ void fold_tile(double* R, double* T, int rows, int ld, int n, double*
   }
 }
 
+// fold_tile for a leaf tile of exactly blockDim.x rows (thread i owns row
+// i): the same Householder arithmetic in the same order — bit-identical —
+// with two barriers per column instead of four (column j+1's norm is
+// reduced by the threads that just updated it, inside column j's update
+// phase) and no per-element index division in the update.
+__device__ void fold_tile_leaf(double* R, double* T, int ld, int n, double* red, double* wbuf) {
+  const int i = threadIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto warp_sq = [&](int col) {
+    const double t = T[col * ld + i];
+    double v = t * t;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+  };
+  warp_sq(0);
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    double sig2 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sig2 += red[w];
+    if (sig2 == 0.0) {  // column already reduced: H = I
+      __syncthreads();  // every thread has read red
+      if (j + 1 < n) warp_sq(j + 1);
+      __syncthreads();
+      continue;
+    }
+    const double alpha = R[j * n + j];
+    const double nrm = sqrt(fma(alpha, alpha, sig2));
+    const double beta = alpha >= 0.0 ? -nrm : nrm;
+    const double v0 = alpha - beta;
+    const double tau = (beta - alpha) / beta;
+    const double inv_v0 = 1.0 / v0;
+    // w_k = R[j][k] + sum_i v_i T[i][k], v_i = T[i][j] / v0, for k > j
+    for (int k = j + 1 + warp; k < n; k += kFitWarps) {
+      double d = 0.0;
+      for (int r = lane; r < (int)blockDim.x; r += 32) d = fma(T[j * ld + r], T[k * ld + r], d);
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      if (lane == 0) wbuf[k] = fma(d, inv_v0, R[j * n + k]);
+    }
+    __syncthreads();  // wbuf complete; red read by every thread
+    if (i == 0) R[j * n + j] = beta;
+    for (int k = j + 1 + i; k < n; k += blockDim.x) R[j * n + k] -= tau * wbuf[k];
+    const double vi = T[j * ld + i] * inv_v0;
+    for (int k = j + 1; k < n; ++k) T[k * ld + i] -= (tau * wbuf[k]) * vi;
+    if (j + 1 < n) warp_sq(j + 1);
+    __syncthreads();
+  }
+}
+
 // eval_monomial (polyfit.hpp:96-105) for one sample and exponent row.
 __device__ __forceinline__ double monomial(const double (&x)[RPG_MAX_VARS], const uint8_t* e, int nv) {
   // Unrolled over the variables so x stays in registers (a runtime index
@@ -184,7 +231,8 @@ tsqr_tiles(const FitParams F, double* __restrict__ Rout) {
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     build_tile(F, t * kTile, T, sexps);
     __syncthreads();
-    fold_tile(R, T, kTile, kTile, ncols, red, wbuf);
+    if (kTile == kFitThreads) fold_tile_leaf(R, T, kTile, ncols, red, wbuf);
+    else fold_tile(R, T, kTile, kTile, ncols, red, wbuf);
   }
   __syncthreads();
   double* out = Rout + (size_t)blockIdx.x * ncols * ncols;
