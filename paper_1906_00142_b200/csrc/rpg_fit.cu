@@ -149,18 +149,49 @@ __device__ void fold_tile_leaf(double* R, double* T, int ld, int n, double* red,
     const double v0 = alpha - beta;
     const double tau = (beta - alpha) / beta;
     const double inv_v0 = 1.0 / v0;
-    // w_k = R[j][k] + sum_i v_i T[i][k], v_i = T[i][j] / v0, for k > j
-    for (int k = j + 1 + warp; k < n; k += kFitWarps) {
-      double d = 0.0;
-      for (int r = lane; r < (int)blockDim.x; r += 32) d = fma(T[j * ld + r], T[k * ld + r], d);
-      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-      if (lane == 0) wbuf[k] = fma(d, inv_v0, R[j * n + k]);
+    // w_k = R[j][k] + sum_i v_i T[i][k], v_i = T[i][j] / v0, for k > j:
+    // warp per k, two k per pass (independent chains), the lane's rows of
+    // column j in registers; per k the row order and shuffle tree of
+    // fold_tile.
+    constexpr int kRows = kFitThreads / 32;
+    double tj[kRows];
+#pragma unroll
+    for (int rr = 0; rr < kRows; ++rr) tj[rr] = T[j * ld + lane + 32 * rr];
+    for (int k = j + 1 + warp; k < n; k += 2 * kFitWarps) {
+      const int k2 = k + kFitWarps;
+      const bool two = k2 < n;
+      const int kk2 = two ? k2 : k;
+      double d = 0.0, d2 = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < kRows; ++rr) {
+        d = fma(tj[rr], T[k * ld + lane + 32 * rr], d);
+        d2 = fma(tj[rr], T[kk2 * ld + lane + 32 * rr], d2);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+        d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+      }
+      if (lane == 0) {
+        wbuf[k] = fma(d, inv_v0, R[j * n + k]);
+        if (two) wbuf[k2] = fma(d2, inv_v0, R[j * n + k2]);
+      }
     }
     __syncthreads();  // wbuf complete; red read by every thread
     if (i == 0) R[j * n + j] = beta;
     for (int k = j + 1 + i; k < n; k += blockDim.x) R[j * n + k] -= tau * wbuf[k];
     const double vi = T[j * ld + i] * inv_v0;
-    for (int k = j + 1; k < n; ++k) T[k * ld + i] -= (tau * wbuf[k]) * vi;
+    int k = j + 1;
+    for (; k + 4 <= n; k += 4) {  // four independent updates per pass
+      double t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[u] = T[(k + u) * ld + i];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[u] -= (tau * wbuf[k + u]) * vi;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) T[(k + u) * ld + i] = t[u];
+    }
+    for (; k < n; ++k) T[k * ld + i] -= (tau * wbuf[k]) * vi;
     if (j + 1 < n) warp_sq(j + 1);
     __syncthreads();
   }

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Fit: two-barrier TSQR leaf fold — bit A/B vs the previous commit, timings.
+# Fit: TSQR leaf fold variants — bit A/B vs build/head_librpgpu.so, timings, tsqr ncu.
 set -u
 O=gpurun_out/${1:-r02ac}; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build rc=$?"
