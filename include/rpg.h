@@ -358,6 +358,15 @@ int64_t rpg_emit_program_cuda_source(const rpg_program* prog, const rpg_profile*
  * failing tuple/configuration), or RPG_OK.  No-op for metric-spec plans. */
 int rpg_plan_poll_error(rpg_plan* plan, void* stream, char* err, size_t errlen);
 
+/* FAST_CM range certificate (diagnostics).  counts[64 m + k] = number of the
+ * plan's configurations for which, for every N in [2^k, 2^(k+1)] (k = 0..63),
+ * pass 1's point is proven to stay on the division fast paths (m = 0: the
+ * search kernel skips the per-point range checks there) and, for m = 1, 2, 3,
+ * also to fall in MWP-CWP case cwp_bound, mwp_bound, both_saturated (the
+ * kernel then evaluates only that case).  Results are identical either way.
+ * All zero when the plan has no certificate (not FAST_CM, or RPG_CM_CERT=0). */
+int rpg_plan_cert_counts(rpg_plan* plan, int64_t counts[256], char* err, size_t errlen);
+
 /* search_optimal over a per-tuple subset of the plan's configuration space
  * (sanity_report searches each data tuple over its own sampled
  * configurations, pipeline.hpp:816-824): tuple t searches the space indices

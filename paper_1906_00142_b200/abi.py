@@ -259,6 +259,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                               C.POINTER(rpg_options), C.c_int32,
                                               C.POINTER(C.c_void_p)) + errbuf),
         "rpg_plan_poll_error": (C.c_int, (C.c_void_p, C.c_void_p) + errbuf),
+        "rpg_plan_cert_counts": (C.c_int, (C.c_void_p, C.POINTER(C.c_int64)) + errbuf),
         "rpg_emit_program_cuda_source": (C.c_int64, (C.c_void_p, C.POINTER(rpg_profile),
                                                      C.POINTER(rpg_options), C.c_int32,
                                                      C.c_char_p, C.c_size_t,
@@ -336,7 +337,7 @@ EXPORTED_SYMBOLS = ("rpg_version", "rpg_device_count", "rpg_plan_create",
                     "rpg_search_batch_group", "rpg_fit_rational_traced", "rpg_fit_rational_multi",
                     "rpg_samples_parse", "rpg_samples_info", "rpg_samples_metric_name",
                     "rpg_samples_copy", "rpg_samples_free", "rpg_samples_format",
-                    "rpg_mwpcwp_breakdown_batch")
+                    "rpg_mwpcwp_breakdown_batch", "rpg_plan_cert_counts")
 
 
 class RpgError(RuntimeError):

@@ -32,6 +32,7 @@ int cm_j();
 // fast_cm plans: the branch-free pass-1 body search_body_cmj (RPG_CM_SCAN=0
 // selects the round-1 bodies search_body_cm / search_body_cm2, J <= 2).
 int cm_scan();
+int cm_cert();
 // fast_cm plans: resident CTAs per SM the kernel is register-budgeted for.
 int cm_min_blocks(int threads, int j);
 

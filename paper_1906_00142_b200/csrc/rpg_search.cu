@@ -69,6 +69,37 @@ __global__ void occ_table_kernel(const __grid_constant__ Params P, int4* __restr
   }
 }
 
+// One warp per (configuration, half): lane k of half h certifies binade
+// 32 h + k (N in [2^(32h+k), 2^(32h+k+1)]) of configuration c.  Layout:
+// cert[4c + m % 4] = mask of the binades where scan mode m (kScanFree,
+// kScanCwp, kScanMwp, kScanBoth) is proven.
+__global__ void __launch_bounds__(256) cm_cert_kernel(const __grid_constant__ Params P,
+                                                      unsigned long long* __restrict__ cert) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int c = warp >> 1, half = warp & 1;
+  if (c >= P.n_space) return;
+  const int k = 32 * half + lane;
+  const int4 rec = P.lean[c];
+  const int b = (int)((unsigned)rec.y >> 16), W = rec.z & 0xffff;
+  // The binade is proven piecewise: kCertPieces sub-boxes (exact bounds: the
+  // width is a power of two) keep the enclosures' dependency overestimate
+  // small; a mode holds on the binade iff it holds on every piece.
+  constexpr int kCertPieces = 16;
+  unsigned modes = 0u;
+  if (k < 62) {
+    const double* row = P.cm + (size_t)c * P.n_cm;
+    const double lo = ldexp(1.0, k), step = ldexp(1.0, k - 4);
+    modes = ~0u;
+    for (int s = 0; s < kCertPieces && modes != 0u; ++s)
+      modes &= cm_certify(P, row, b, W, lo + s * step, lo + (s + 1) * step);
+  }
+  unsigned* out = reinterpret_cast<unsigned*>(cert + 4 * (size_t)c);
+  for (int m = kScanFree; m <= kScanBoth; ++m) {
+    const unsigned bits = __ballot_sync(0xffffffffu, (modes >> m) & 1u);
+    if (lane == 0) out[2 * (m % 4) + half] = bits;
+  }
+}
+
 // RPG_ARITH_FAST_CM table: per configuration and metric polynomial, the
 // coefficient of each power of D1, C_j = fma(c_k, mB_k, C_j) over the terms
 // in basis order, mB_k = the product over the block variables in model
@@ -185,6 +216,7 @@ struct rpg_plan {
   int4* d_lean = nullptr;
   double2* d_rep_tab = nullptr;
   double* d_cm = nullptr;      // RPG_ARITH_FAST_CM per-configuration table
+  unsigned long long* d_cert = nullptr;  // FAST_CM range certificate (cm_cert_kernel)
   int tuples_per_cta = 1;      // FAST_CM: 32 tuples (one per lane) per CTA
   // bare-program plans: first evaluation error (Params::err_flag)
   bool is_program = false;
@@ -540,6 +572,13 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     occ_table_kernel<<<(int)((nthr + 255) / 256), 256, 0, plan->stream>>>(
         P, plan->d_occ, plan->d_occ_rcp, plan->d_lean, plan->d_rep_tab);
     PLAN_CUDA(cudaGetLastError());
+    if (P.arith == RPG_ARITH_FAST_CM && P.cm_scan && P.lean && rpg_jit::cm_cert()) {
+      // the pass-1 range certificate: 64 binades of N per configuration
+      PLAN_CUDA(cudaMalloc(&plan->d_cert, 4 * sizeof(unsigned long long) * (size_t)n_space));
+      cm_cert_kernel<<<(int)((n_space * 64 + 255) / 256), 256, 0, plan->stream>>>(P, plan->d_cert);
+      PLAN_CUDA(cudaGetLastError());
+      P.cert = plan->d_cert;
+    }
     PLAN_CUDA(cudaStreamSynchronize(plan->stream));
   }
 
@@ -722,6 +761,7 @@ int rpg_plan_destroy(rpg_plan* plan) {
   cudaFree(plan->d_occ);
   cudaFree(plan->d_occ_rcp);
   cudaFree(plan->d_lean);
+  cudaFree(plan->d_cert);
   cudaFree(plan->d_rep_tab);
   cudaFree(plan->d_err);
   cudaFree(plan->d_data);
@@ -786,6 +826,21 @@ int rpg_plan_poll_error(rpg_plan* plan, void* stream, char* err, size_t errlen) 
   CUDA_TRY(cudaSetDevice(plan->device));
   if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   return take_program_error(plan, err, errlen);
+}
+
+int rpg_plan_cert_counts(rpg_plan* plan, int64_t counts[256], char* err, size_t errlen) {
+  if (!plan || !counts) return set_err(err, errlen, RPG_E_INVALID, "null plan or counts");
+  for (int k = 0; k < 256; ++k) counts[k] = 0;
+  if (!plan->d_cert) return RPG_OK;
+  std::lock_guard<std::mutex> lock(plan->mu);
+  CUDA_TRY(cudaSetDevice(plan->device));
+  std::vector<unsigned long long> h(4 * (size_t)plan->P.n_space);
+  CUDA_TRY(cudaMemcpy(h.data(), plan->d_cert, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+  static const int slot[4] = {kScanFree % 4, kScanCwp % 4, kScanMwp % 4, kScanBoth % 4};
+  for (size_t c = 0; c < (size_t)plan->P.n_space; ++c)
+    for (int m = 0; m < 4; ++m)
+      for (int k = 0; k < 64; ++k) counts[64 * m + k] += (h[4 * c + slot[m]] >> k) & 1ull;
+  return RPG_OK;
 }
 
 }  // extern "C"

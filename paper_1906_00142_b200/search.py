@@ -145,6 +145,17 @@ class Plan:
         self._check(self.lib.rpg_plan_poll_error(self._handle, C.c_void_p(stream_ptr),
                                                  err, len(err)), err)
 
+    def cert_counts(self) -> dict:
+        """FAST_CM range certificate (rpg_plan_cert_counts): for each binade k
+        of N ([2^k, 2^(k+1)]), how many configurations run pass 1 without
+        per-point range checks ("free") and with the MWP-CWP case proven
+        ("cwp", "mwp", "both").  All zero without a certificate."""
+        out = (C.c_int64 * 256)()
+        err = C.create_string_buffer(512)
+        self._check(self.lib.rpg_plan_cert_counts(self._handle, out, err, len(err)), err)
+        v = list(out)
+        return {name: v[64 * m:64 * (m + 1)] for m, name in enumerate(("free", "cwp", "mwp", "both"))}
+
     def close(self) -> None:
         if self._handle:
             self.lib.rpg_plan_destroy(self._handle)
