@@ -14,6 +14,9 @@ struct Module {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t search = nullptr;
   cudaKernel_t evaluate = nullptr;
+  // fast_cm with J = 3: the same search with J = 2 (64-tuple groups), picked
+  // per launch when the batch fills the grid's waves better with it
+  cudaKernel_t search_alt = nullptr;
   size_t cubin_bytes = 0;
 };
 

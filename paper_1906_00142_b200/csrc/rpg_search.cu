@@ -626,6 +626,10 @@ int build_plan(Params& P, const ModelTables& tab, const rpg_config* space, int64
     return cudaSuccess;
   };
   PLAN_CUDA(setup(search_fn(plan), &plan->grid_search));
+  if (plan->specialized && plan->jit.search_alt) {
+    int g = 0;
+    PLAN_CUDA(setup(reinterpret_cast<const void*>(plan->jit.search_alt), &g));
+  }
   PLAN_CUDA(setup(evaluate_fn(plan), &plan->grid_eval));
   plan->P = P;
 #undef PLAN_CUDA
@@ -873,10 +877,27 @@ int launch_search(rpg_plan* plan, const int64_t* d_data, int64_t n, int32_t d,
   P.d = d;
   P.sub_off = d_sub_off;
   P.sub_list = d_sub_list;
-  const int64_t units = (n + plan->tuples_per_cta - 1) / plan->tuples_per_cta;
+  const void* fn = search_fn(plan);
+  int64_t per_unit = plan->tuples_per_cta;
+  if (plan->specialized && plan->jit.search_alt) {
+    // J = 3 (96-tuple groups) or the J = 2 alternate (64): the larger of
+    // rate x wave fill, rate(J=3) / rate(J=2) = 1.117 per full wave
+    // (profiles/r02s3_j_sweep.txt); strong-scaled shards of C2 over 2-8 GPUs
+    // take J = 2, the 1-GPU step J = 3.
+    auto fill = [&](int64_t tuples_per_unit) {
+      const double w = (double)((n + tuples_per_unit - 1) / tuples_per_unit) / plan->grid_search;
+      return w / std::ceil(w);
+    };
+    const int64_t alt = plan->tuples_per_cta / 3 * 2;
+    if (fill(alt) > 1.117 * fill(plan->tuples_per_cta)) {
+      fn = reinterpret_cast<const void*>(plan->jit.search_alt);
+      per_unit = alt;
+    }
+  }
+  const int64_t units = (n + per_unit - 1) / per_unit;
   const int grid = (int)std::min<int64_t>(units, plan->grid_search);
   void* args[] = {&P, &d_data, &n, &d_out};
-  CUDA_TRY(cudaLaunchKernel(search_fn(plan), dim3(grid), dim3(plan->threads), args, plan->smem, s));
+  CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(plan->threads), args, plan->smem, s));
   return RPG_OK;
 }
 
