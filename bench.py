@@ -340,7 +340,14 @@ def gpu_arm(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
-    launches_per_step = len(wl.kernels)
+    def search_only():
+        for k in wl.kernels:
+            plans[k].search_batch_device(data_dev.data_ptr(), n, d, out_dev[k].data_ptr(), sptr)
+
+    # rpg_* kernels one step launches (a FAST_CM batch may run as J = 3 full
+    # waves + a J = 2 remainder), counted by the CUDA activity trace outside
+    # the timed region; one launch per kernel model if tracing is unavailable
+    launches_per_step = count_kernel_launches(search_only) or len(wl.kernels)
 
     def step():
         for k in wl.kernels:

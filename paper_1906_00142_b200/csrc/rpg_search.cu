@@ -877,27 +877,39 @@ int launch_search(rpg_plan* plan, const int64_t* d_data, int64_t n, int32_t d,
   P.d = d;
   P.sub_off = d_sub_off;
   P.sub_list = d_sub_list;
-  const void* fn = search_fn(plan);
-  int64_t per_unit = plan->tuples_per_cta;
+  auto launch = [&](const void* fn, const int64_t* dd, int64_t cnt, rpg_winner* o,
+                    int64_t per_unit) -> cudaError_t {
+    const int64_t units = (cnt + per_unit - 1) / per_unit;
+    const int grid = (int)std::min<int64_t>(units, plan->grid_search);
+    void* args[] = {&P, &dd, &cnt, &o};
+    return cudaLaunchKernel(fn, dim3(grid), dim3(plan->threads), args, plan->smem, s);
+  };
   if (plan->specialized && plan->jit.search_alt) {
-    // J = 3 (96-tuple groups) or the J = 2 alternate (64): the larger of
-    // rate x wave fill, rate(J=3) / rate(J=2) = 1.117 per full wave
-    // (profiles/r02s3_j_sweep.txt); strong-scaled shards of C2 over 2-8 GPUs
-    // take J = 2, the 1-GPU step J = 3.
-    auto fill = [&](int64_t tuples_per_unit) {
-      const double w = (double)((n + tuples_per_unit - 1) / tuples_per_unit) / plan->grid_search;
-      return w / std::ceil(w);
-    };
-    const int64_t alt = plan->tuples_per_cta / 3 * 2;
-    if (fill(alt) > 1.117 * fill(plan->tuples_per_cta)) {
-      fn = reinterpret_cast<const void*>(plan->jit.search_alt);
-      per_unit = alt;
+    // J = 3 (96-tuple groups) and the J = 2 alternate (64): the whole batch
+    // with either, or the J = 3 full waves followed by the rest with J = 2,
+    // whichever takes the fewest J = 3 wave-times — a J = 2 wave takes
+    // (64 / 96) x 1.117 of one (rate(J=3) / rate(J=2) = 1.117 per full wave,
+    // profiles/r02s3_j_sweep.txt).  The 1-GPU C2 step runs 4 J = 3 waves +
+    // one J = 2 wave instead of 4.6 J = 3 waves; strong-scaled shards of it
+    // on 2-8 GPUs run J = 2.
+    const int64_t t3 = plan->tuples_per_cta, t2 = t3 / 3 * 2, g = plan->grid_search;
+    const double w2 = (double)t2 / (double)t3 * 1.117;
+    const int64_t full3 = n / (t3 * g) * (t3 * g), rest = n - full3;
+    const double c_all3 = (double)((n + t3 * g - 1) / (t3 * g));
+    const double c_all2 = w2 * (double)((n + t2 * g - 1) / (t2 * g));
+    const double c_split = (double)(full3 / (t3 * g)) + w2 * (double)((rest + t2 * g - 1) / (t2 * g));
+    const void* alt = reinterpret_cast<const void*>(plan->jit.search_alt);
+    if (c_split < c_all3 && c_split <= c_all2 && full3 > 0 && rest > 0) {
+      CUDA_TRY(launch(search_fn(plan), d_data, full3, d_out, t3));
+      CUDA_TRY(launch(alt, d_data + full3 * d, rest, d_out + full3, t2));
+    } else if (c_all2 < c_all3) {
+      CUDA_TRY(launch(alt, d_data, n, d_out, t2));
+    } else {
+      CUDA_TRY(launch(search_fn(plan), d_data, n, d_out, t3));
     }
+    return RPG_OK;
   }
-  const int64_t units = (n + per_unit - 1) / per_unit;
-  const int grid = (int)std::min<int64_t>(units, plan->grid_search);
-  void* args[] = {&P, &d_data, &n, &d_out};
-  CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(plan->threads), args, plan->smem, s));
+  CUDA_TRY(launch(search_fn(plan), d_data, n, d_out, plan->tuples_per_cta));
   return RPG_OK;
 }
 
