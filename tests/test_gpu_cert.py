@@ -126,3 +126,23 @@ def test_cert_counts():
         assert all(c[m][k] <= c["free"][k] for k in range(64))
     with S.Plan(_spec(CASES["gemm"]), hw, space, S.SearchOptions(arith="fast")) as plan:
         assert all(v == 0 for m in plan.cert_counts().values() for v in m)
+
+
+@pytest.mark.parametrize("kernel", ["c6_stencil", "c6_kloop", "c6_reduce"])
+def test_cert_dump_table_c6(kernel):
+    """The Ec dump (rpg_evaluate, FAST_CM) takes the certificate's proven case
+    as the point's tag (finish_point_cert): the whole table — Ec, tag,
+    occupancy — bit-identical to O1's FAST_CM twin on the landscape with all
+    three cases, infeasible configurations and exact ties."""
+    from oracle import o1
+    from paper_1906_00142_b200 import abi as A
+    spec, hw, space = _spec(CASES[kernel]), _hw(), F.integer_configs(1024, dims=2)
+    data = np.arange(64, 65537, 3637, dtype=np.int64).reshape(-1, 1)
+    opts = S.SearchOptions(arith="fastcm")
+    with S.Plan(spec, hw, space, opts) as plan:
+        ec, tag, wocc = plan.evaluate(data)
+    oec, otag, owocc = o1.evaluate_batch(A.PackedModel(spec, drop_zero_terms=False), A.profile_struct(hw),
+                                         opts.struct(), A.config_array(space), data, os.cpu_count() or 1)
+    assert np.array_equal(ec.view(np.int64), oec.view(np.int64))
+    assert np.array_equal(tag, otag) and np.array_equal(wocc, owocc)
+    assert len(np.unique(tag)) >= 3  # the three cases (plus infeasible points) are in the table

@@ -44,6 +44,14 @@ def main():
     data = np.arange(64, 65537, 1021, dtype=np.int64).reshape(-1, 1)[:48]
     ok = True
     ok &= check("gemm fastcm (pair)", gemm, hw, space2, data, arith="fastcm")
+    # one full J = 3 wave on 148 SMs (96-tuple groups) + a J = 2 remainder,
+    # certified bodies (range certificate)
+    big = np.arange(64, 64 + 148 * 96 + 100, dtype=np.int64).reshape(-1, 1)
+    ok &= check("gemm fastcm (J=3 wave + J=2 rest)", gemm, hw, space2[::5], big, arith="fastcm")
+    for k in ("c6_stencil", "c6_reduce"):  # all three proven-case bodies, infeasible configs, ties
+        c6 = F.models_to_metric_spec(F.read_models(os.path.join(ROOT, "data", "stressed", f"{k}.models.json")))
+        ok &= check(f"{k} fastcm", c6, F.load_profile(os.path.join(ROOT, "data", "b200.profile")), space2, data,
+                    arith="fastcm")
     ok &= check("gemm fast specialized", gemm, hw, space2, data[:16], arith="fast")
     ok &= check("gemm exact specialized", gemm, hw, space2, data[:8], arith="exact")
     ok &= check("gemm fast generic", gemm, hw, space2, data[:8], arith="fast", kernel="generic")
